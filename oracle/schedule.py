@@ -1,0 +1,101 @@
+"""Noise schedule, DDIM update, classifier-free guidance, band-row rule.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+* CFG, Eq. 2 (§3.1): eps_hat = eps_u + s (eps_c - eps_u), s = 5 (§4).
+* Sampler: "50-step DDIM sampler" (§4).  The paper gives no schedule;
+  reading D2: SDXL's public scheduler configuration --
+  scaled_linear betas in [0.00085, 0.012] over 1000 training steps,
+  'leading' spacing with steps_offset 1, final alpha_bar_prev = alpha_bar[0],
+  eta = 0 (deterministic, no noise).
+* Eq. 3-4: DDPM ancestral mean; provided for the closed-form pin that
+  ties alpha, beta and alpha_bar together (not used by the DDIM sampler).
+* rows(p, h): Eq. 1 takes "p h" rows of a neighbour; reading D1:
+  floor(p h + 1e-9), at least one row when p > 0, at most h.
+
+Pins (tests/test_oracle_schedule.py): alpha_bar = prod(1 - beta); DDIM step on
+an exact x_tau = sqrt(ab) x0 + sqrt(1-ab) eps returns sqrt(ab') x0 +
+sqrt(1-ab') eps; CFG identities s=1 -> eps_c, eps_c = eps_u -> eps_u; the
+printed p values of Fig. 4 give integer row counts.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+NUM_TRAIN_TIMESTEPS = 1000
+BETA_START = 0.00085
+BETA_END = 0.012
+
+
+def betas() -> np.ndarray:
+    """scaled_linear: beta_t = (linspace(sqrt(b0), sqrt(b1), 1000))^2, t = 0..999."""
+    return np.linspace(math.sqrt(BETA_START), math.sqrt(BETA_END),
+                       NUM_TRAIN_TIMESTEPS, dtype=np.float64) ** 2
+
+
+def alpha_bars() -> np.ndarray:
+    """alpha_bar_t = prod_{s<=t} (1 - beta_s)  (P:70 'ᾱ_t = Π α_s')."""
+    a = 1.0 - betas()
+    out = np.empty_like(a)
+    acc = 1.0
+    for t in range(a.shape[0]):       # explicit running product, no cumprod
+        acc *= a[t]
+        out[t] = acc
+    return out
+
+
+def ddim_timesteps(num_steps: int) -> list[int]:
+    """'leading' spacing with steps_offset=1: tau_k = (S-1-k)*(1000//S) + 1."""
+    ratio = NUM_TRAIN_TIMESTEPS // num_steps
+    return [(num_steps - 1 - k) * ratio + 1 for k in range(num_steps)]
+
+
+def ddim_coeffs(num_steps: int, k: int) -> tuple[float, float, float, float]:
+    """(alpha_bar_tau, alpha_bar_prev) -> the four DDIM scalars for step k.
+
+    Returns (sqrt(ab), sqrt(1-ab), sqrt(ab_prev), sqrt(1-ab_prev)).
+    prev timestep = tau - 1000//S; alpha_bar_prev = alpha_bar[0] when prev < 0
+    (set_alpha_to_one = False, reading D2).
+    """
+    ab = alpha_bars()
+    tau = ddim_timesteps(num_steps)[k]
+    prev = tau - NUM_TRAIN_TIMESTEPS // num_steps
+    a_t = ab[tau]
+    a_p = ab[prev] if prev >= 0 else ab[0]
+    return math.sqrt(a_t), math.sqrt(1.0 - a_t), math.sqrt(a_p), math.sqrt(1.0 - a_p)
+
+
+def cfg_combine(eps_u: np.ndarray, eps_c: np.ndarray, s: float) -> np.ndarray:
+    """Eq. 2: eps_hat = eps_u + s (eps_c - eps_u)."""
+    return eps_u + s * (eps_c - eps_u)
+
+
+def ddim_step(x: np.ndarray, eps_hat: np.ndarray, num_steps: int, k: int) -> np.ndarray:
+    """Deterministic DDIM (eta = 0) update for step k (P:134 '50-step DDIM').
+
+    x0_hat = (x - sqrt(1-ab) eps) / sqrt(ab);  x' = sqrt(ab') x0_hat + sqrt(1-ab') eps.
+    """
+    sa, s1a, sp, s1p = ddim_coeffs(num_steps, k)
+    x0 = (x - s1a * eps_hat) / sa
+    return sp * x0 + s1p * eps_hat
+
+
+def ddpm_mean(x: np.ndarray, eps_hat: np.ndarray, t: int) -> np.ndarray:
+    """Eq. 3: mu = (x_t - beta_t / sqrt(1 - ab_t) eps_hat) / sqrt(alpha_t)."""
+    b = betas()[t]
+    ab = alpha_bars()[t]
+    return (x - b / math.sqrt(1.0 - ab) * eps_hat) / math.sqrt(1.0 - b)
+
+
+def band_rows(p: float, h: int) -> int:
+    """Eq. 1 'upper/lower p h of' a neighbour patch of height h.
+
+    Reading D1: 0 if p == 0, else min(h, max(1, floor(p h + 1e-9))).
+    """
+    if not (0.0 <= p <= 1.0):
+        raise ValueError("p must lie in [0, 1] (p > 1 is undefined, P:209 §6)")
+    if p == 0.0:
+        return 0
+    return min(h, max(1, int(math.floor(p * h + 1e-9))))

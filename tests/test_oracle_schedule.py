@@ -1,0 +1,89 @@
+"""Pins for oracle/schedule.py against closed forms and the paper's numbers."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import schedule as S
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_alpha_bar_is_product_of_alphas():
+    # P:70 §3.1: alpha_bar_t = prod_{s<=t} alpha_s; checked against numpy's cumprod
+    b = S.betas()
+    assert b.shape == (1000,)
+    assert np.all(np.diff(b) > 0) and 0 < b[0] < b[-1] < 1
+    np.testing.assert_allclose(S.alpha_bars(), np.cumprod(1.0 - b), rtol=1e-12)
+    # scaled_linear endpoints (reading D2)
+    assert math.isclose(b[0], 0.00085, rel_tol=1e-12) and math.isclose(b[-1], 0.012, rel_tol=1e-12)
+
+
+def test_ddim_timesteps_leading_spacing():
+    assert S.ddim_timesteps(4) == [751, 501, 251, 1]
+    t50 = S.ddim_timesteps(json.load(open(os.path.join(GOLD, "paper_settings.json")))["ddim_steps"]["value"])
+    assert len(t50) == 50 and t50[0] == 981 and t50[-1] == 1 and all(a - b == 20 for a, b in zip(t50, t50[1:]))
+
+
+@pytest.mark.parametrize("steps", [4, 50])
+def test_ddim_step_closed_form(steps):
+    # P8: feeding the exact noise back reproduces the forward-marginal at tau_prev
+    rng = np.random.default_rng(0)
+    x0 = rng.standard_normal((8, 8, 4))
+    eps = rng.standard_normal((8, 8, 4))
+    ab = S.alpha_bars()
+    taus = S.ddim_timesteps(steps)
+    for k, tau in enumerate(taus):
+        x = math.sqrt(ab[tau]) * x0 + math.sqrt(1 - ab[tau]) * eps
+        prev = tau - 1000 // steps
+        ap = ab[prev] if prev >= 0 else ab[0]
+        want = math.sqrt(ap) * x0 + math.sqrt(1 - ap) * eps
+        np.testing.assert_allclose(S.ddim_step(x, eps, steps, k), want, atol=1e-12, rtol=0)
+
+
+def test_cfg_identities():
+    rng = np.random.default_rng(1)
+    u, c = rng.standard_normal(16), rng.standard_normal(16)
+    np.testing.assert_allclose(S.cfg_combine(u, c, 1.0), c, atol=1e-15)   # s = 1 -> eps_c
+    np.testing.assert_array_equal(S.cfg_combine(u, u, 5.0), u)          # eps_c = eps_u -> eps_u
+    np.testing.assert_allclose(S.cfg_combine(np.zeros(16), c, 5.0), 5 * c)  # s = 5
+    # linearity: cfg(a,b,s) + cfg(b,a,s) = a + b
+    np.testing.assert_allclose(S.cfg_combine(u, c, 5.0) + S.cfg_combine(c, u, 5.0), u + c, atol=1e-12)
+
+
+def test_ddpm_mean_closed_form():
+    # Eq. 3 with eps_hat = 0 is x / sqrt(alpha_t); with x = sqrt(ab) x0 + sqrt(1-ab) eps and
+    # eps_hat = eps it equals the posterior mean coefficient form (Ho et al. Eq. 11)
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal(10)
+    t = 500
+    a = 1 - S.betas()[t]
+    np.testing.assert_allclose(S.ddpm_mean(x, np.zeros(10), t), x / math.sqrt(a), rtol=1e-14)
+    x0, e = rng.standard_normal(10), rng.standard_normal(10)
+    ab, abp = S.alpha_bars()[t], S.alpha_bars()[t - 1]
+    xt = math.sqrt(ab) * x0 + math.sqrt(1 - ab) * e
+    b = S.betas()[t]
+    post = (math.sqrt(abp) * b / (1 - ab)) * x0 + (math.sqrt(a) * (1 - abp) / (1 - ab)) * xt
+    np.testing.assert_allclose(S.ddpm_mean(xt, e, t), post, atol=1e-12)
+
+
+def test_band_rows_rule():
+    # Eq. 1 'p h' rows; reading D1: floor with 1e-9 guard, >=1 when p>0, <=h
+    assert S.band_rows(0.0, 16) == 0
+    assert S.band_rows(0.25, 16) == 4
+    assert S.band_rows(1.0, 16) == 16
+    assert S.band_rows(0.3, 10) == 3          # 0.3*10 = 2.9999999999999996 in binary
+    assert S.band_rows(0.01, 4) == 1
+    assert S.band_rows(0.8, 8) == 6 and S.band_rows(0.8, 4) == 3
+    for h in range(1, 129):
+        prev = 0
+        for k in range(0, 1001):
+            r = S.band_rows(k / 1000, h)
+            assert 0 <= r <= h and r >= prev          # monotone in p
+            if k:
+                assert r == min(h, max(1, (k * h) // 1000))   # exact integer form of floor(p h)
+            prev = r
+    with pytest.raises(ValueError):
+        S.band_rows(1.5, 8)                       # p > 1 undefined
