@@ -15,6 +15,7 @@ Two conventions:
        attn  PCPP async   : 2 (n-1) r_l W_l 2 C_l B e
        attn  warm-up / FULLMAP: (n-1) H_l W_l 2 C_l B e
        conv  stride 1     : 2 (n-1) W_in C_in B e ;  stride 2: (n-1) W_in C_in B e
+                            (conv_in's input is the fp32 latent: e = 4 there)
        gn    (all-gather of local sums, float64): n (n-1) 2 G B 8
    Pinned by the oracle's counted ledger (pcpp.sample) on every config.
 """
@@ -112,7 +113,8 @@ def physical_bytes(model: str, H: int, W: int, n: int, p: float, elem_bytes: int
                 tot["attn"] += (n - 1) * Hl * Wl * 2 * C * B_CFG * elem_bytes
         elif L["kind"] == "conv":
             mult = 2 if L["stride"] == 1 else 1
-            tot["conv"] += mult * (n - 1) * L["W_l"] * L["C"] * B_CFG * elem_bytes
+            e = 4 if L["C"] == 4 else elem_bytes          # conv_in reads the fp32 latent (reading D9)
+            tot["conv"] += mult * (n - 1) * L["W_l"] * L["C"] * B_CFG * e
         else:
             tot["gn"] += n * (n - 1) * 2 * M.G_GROUPS * B_CFG * 8
     return tot

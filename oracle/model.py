@@ -314,7 +314,8 @@ def group_norm(ctx: Ctx, xs, gamma, beta, act: bool):
     for i, x in enumerate(xs):
         for j in range(n):
             ctx.read("gn", lid, j, i, ms[j].size)
-        if ctx.mode in ("sync", "fresh"):
+        if ctx.mode in ("sync", "fresh") or n == 1:
+            # n = 1: M_{t+1} - m_{0,t+1} + m_0 = m_0 = M_fresh exactly (no other rank exists)
             M = M_fresh
         else:
             M = ctx.prev[(lid, "M")] - ctx.prev[(lid, "m")][i] + ms[i]

@@ -95,8 +95,10 @@ def forward_pair(cfg: Config, blob, x, tau, cond, first_mode: str, second_mode: 
 
 def ledger_totals(entries, elem_bytes: int) -> dict:
     """Sum a step's counted ledger into bytes per class.  Activations travel at
-    elem_bytes per element; GN statistics as float64 (8 bytes)."""
+    elem_bytes per element, the latent halos of conv_in at 4 (fp32), GN statistics
+    as float64 (8 bytes)."""
     tot = {"attn": 0, "conv": 0, "gn": 0}
-    for kind, _lid, _src, _dst, elems in entries:
-        tot[kind] += elems * (8 if kind == "gn" else elem_bytes)
+    for kind, lid, _src, _dst, elems in entries:
+        e = 8 if kind == "gn" else (4 if lid == "conv0" else elem_bytes)   # conv0 = conv_in on the fp32 latent
+        tot[kind] += elems * e
     return tot

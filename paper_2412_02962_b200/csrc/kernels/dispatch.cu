@@ -1,0 +1,33 @@
+// Kernel selection: tcgen05 (sm_100a tensor cores) for the bf16 contractions the TC kernels
+// support, SIMT otherwise (fp32 parity mode, conv_in, odd shapes).
+#include "../common.cuh"
+#include "../kernels.h"
+#include "../runtime/runtime.h"
+
+namespace pcpp {
+
+bool tc_available();
+bool gemm_tc_supported(const GemmArgs& g);
+bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
+void gemm_tc_init();
+
+void launch_gemm_auto(const GemmArgs& g, bool allow_tc, cudaStream_t s) {
+  if (allow_tc && gemm_tc_supported(g) && launch_gemm_tc(g, s)) return;
+  launch_gemm_simt(g, s);
+}
+void launch_attn_auto(const AttnArgs& a, bool allow_tc, cudaStream_t s) {
+  (void)allow_tc;
+  launch_attn_simt(a, s);
+}
+void launch_gemm_tc_or_simt(const Plan& P, const GemmArgs& g, cudaStream_t s) { launch_gemm_auto(g, P.use_tc, s); }
+void launch_attn_tc_or_simt(const Plan& P, const AttnArgs& a, cudaStream_t s) { launch_attn_auto(a, P.use_tc, s); }
+
+void kernels_init() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  gn_init();
+  gemm_tc_init();
+}
+
+}  // namespace pcpp

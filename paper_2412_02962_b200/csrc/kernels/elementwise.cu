@@ -1,0 +1,167 @@
+// HBM-/launch-bound elementwise kernels of the step: latent prep, nearest upsample, the fused
+// CFG (Eq. 2) + DDIM update, the timestep embedding, and the pack/unpack
+// segment copier used for band staging and the loopback exchange.
+#include "../common.cuh"
+#include "../kernels.h"
+
+namespace pcpp {
+
+// ---- latent [h][W][4] fp32 -> xin [h][2][W][4] fp32 (rows 0..h-1; halos untouched) ------------
+__global__ void prep_latent_kernel(const float4* __restrict__ lat, float4* __restrict__ xin, int h, int W) {
+  const long long n = (long long)h * W;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / W, w = i % W;
+    const float4 v = lat[i];
+    xin[(r * 2 + 0) * W + w] = v;
+    xin[(r * 2 + 1) * W + w] = v;
+  }
+}
+void launch_prep_latent(const float* latent, const ActView& xin, cudaStream_t s) {
+  const long long n = (long long)xin.rows * xin.W;
+  int blocks = (int)((n + 255) / 256); if (blocks > 1184) blocks = 1184;
+  prep_latent_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(latent),
+                                             reinterpret_cast<float4*>(xin.base), xin.rows, xin.W);
+}
+
+// ---- nearest x2 upsample (16-byte vectors) ------------------------------------------------------
+__global__ void upsample2_kernel(const uint4* __restrict__ in, uint4* __restrict__ out,
+                                 int h, int B, int W, int nv /*16B vectors per token*/) {
+  const long long n = (long long)2 * h * B * 2 * W * nv;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(i % nv); long long t = i / nv;
+    const int wo = (int)(t % (2 * W)); t /= (2 * W);
+    const int b = (int)(t % B); const int ro = (int)(t / B);
+    out[i] = in[((((long long)(ro >> 1)) * B + b) * W + (wo >> 1)) * nv + v];
+  }
+}
+void launch_upsample2(const ActView& in, const ActView& out, cudaStream_t s) {
+  const int nv = (int)(in.C * dtype_size(in.dtype) / 16);
+  const long long n = (long long)out.rows * out.B * out.W * nv;
+  int blocks = (int)((n + 255) / 256); if (blocks > 1184 * 2) blocks = 1184 * 2;
+  upsample2_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(in.base), reinterpret_cast<uint4*>(out.base),
+                                          in.rows, in.B, in.W, nv);
+}
+
+// ---- CFG + DDIM -------------------------------------------------------------------------------
+// eps_hat = eps_u + s (eps_c - eps_u);  x0 = (x - sqrt(1-ab) eps_hat)/sqrt(ab);
+// x' = sqrt(ab_prev) x0 + sqrt(1-ab_prev) eps_hat     (b = 0 uncond, b = 1 cond; reading D11)
+__global__ void cfg_ddim_kernel(const float4* __restrict__ eps, float4* __restrict__ lat, int h, int W,
+                                float s_cfg, const double* __restrict__ coef, const int* __restrict__ k_dev) {
+  const int k = *k_dev;
+  const float sa = (float)coef[4 * k + 0], s1a = (float)coef[4 * k + 1];
+  const float sp = (float)coef[4 * k + 2], s1p = (float)coef[4 * k + 3];
+  const float inv_sa = (float)(1.0 / coef[4 * k + 0]);
+  (void)sa;
+  const long long n = (long long)h * W;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / W, w = i % W;
+    const float4 eu = eps[(r * 2 + 0) * W + w], ec = eps[(r * 2 + 1) * W + w];
+    float4 x = lat[i];
+    float e[4] = {eu.x + s_cfg * (ec.x - eu.x), eu.y + s_cfg * (ec.y - eu.y),
+                  eu.z + s_cfg * (ec.z - eu.z), eu.w + s_cfg * (ec.w - eu.w)};
+    float* xv = &x.x;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float x0 = (xv[c] - s1a * e[c]) * inv_sa;
+      xv[c] = sp * x0 + s1p * e[c];
+    }
+    lat[i] = x;
+  }
+}
+void launch_cfg_ddim(const float* eps, float* latent, int h, int W, float s_cfg, const double* coef,
+                     const int* k_dev, cudaStream_t s) {
+  const long long n = (long long)h * W;
+  int blocks = (int)((n + 255) / 256); if (blocks > 1184) blocks = 1184;
+  cfg_ddim_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(eps), reinterpret_cast<float4*>(latent),
+                                         h, W, s_cfg, coef, k_dev);
+}
+
+__global__ void step_end_kernel(int* k_dev) { *k_dev += 1; }
+void launch_step_end(int* k_dev, cudaStream_t s) { step_end_kernel<<<1, 1, 0, s>>>(k_dev); }
+
+// ---- timestep embedding (reading D19) --------------------------------------------------------
+// hid[j] = SiLU(W1[j] . sinusoid(tau) + b1[j]) ; emb[b][j] = W2[j] . hid + b2[j] (+ cond[j] if b = 1)
+__global__ void temb_hidden_kernel(const float* __restrict__ w1, const float* __restrict__ b1,
+                                   const int* __restrict__ taus, const int* __restrict__ k_dev,
+                                   int T, int S, float* __restrict__ hid) {
+  extern __shared__ float e[];
+  const float tau = (float)taus[*k_dev];
+  const int half = S / 2;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    const double f = exp(-log(10000.0) * (double)j / (double)half);
+    const double a = (double)tau * f;
+    e[j] = (float)cos(a);
+    e[half + j] = (float)sin(a);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= T) return;
+  float acc = 0.f;
+  for (int i = lane; i < S; i += 32) acc = fmaf(w1[(long long)row * S + i], e[i], acc);
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if (lane == 0) { const float y = acc + b1[row]; hid[row] = y / (1.f + expf(-y)); }
+}
+__global__ void temb_out_kernel(const float* __restrict__ w2, const float* __restrict__ b2,
+                                const float* __restrict__ cond, const float* __restrict__ hid, int T,
+                                float* __restrict__ emb) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= T) return;
+  float acc = 0.f;
+  for (int i = lane; i < T; i += 32) acc = fmaf(w2[(long long)row * T + i], hid[i], acc);
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if (lane == 0) {
+    const float y = acc + b2[row];
+    emb[row] = y;
+    emb[T + row] = y + cond[row];
+  }
+}
+void launch_temb(const float* w1, const float* b1, const float* w2, const float* b2, const float* cond,
+                 const int* taus, const int* k_dev, int T, int S, float* hid, float* emb, cudaStream_t s) {
+  temb_hidden_kernel<<<(T + 7) / 8, 256, S * sizeof(float), s>>>(w1, b1, taus, k_dev, T, S, hid);
+  temb_out_kernel<<<(T + 7) / 8, 256, 0, s>>>(w2, b2, cond, hid, T, emb);
+}
+// out[b][j] = Wt[j] . SiLU(emb[b]) + bt[j]   for every ResBlock's temb projection at once
+__global__ void temb_proj_kernel(const float* __restrict__ wt, const float* __restrict__ bt,
+                                 const float* __restrict__ emb, int T, int J, float* __restrict__ out) {
+  extern __shared__ float se[];
+  for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) { const float y = emb[i]; se[i] = y / (1.f + expf(-y)); }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= J) return;
+  float a0 = 0.f, a1 = 0.f;
+  for (int i = lane; i < T; i += 32) { const float wv = wt[(long long)row * T + i]; a0 = fmaf(wv, se[i], a0); a1 = fmaf(wv, se[T + i], a1); }
+  for (int d = 16; d > 0; d >>= 1) { a0 += __shfl_xor_sync(0xffffffffu, a0, d); a1 += __shfl_xor_sync(0xffffffffu, a1, d); }
+  if (lane == 0) { out[row] = a0 + bt[row]; out[J + row] = a1 + bt[row]; }
+}
+void launch_temb_proj(const float* wt, const float* bt, const float* emb, int T, int J, float* out, cudaStream_t s) {
+  temb_proj_kernel<<<(J + 7) / 8, 256, 2 * T * sizeof(float), s>>>(wt, bt, emb, T, J, out);
+}
+
+// ---- segment copier: pack / unpack / loopback exchange ------------------------------------------
+// One CTA per segment slice; 16-byte vectors, coalesced.  Segments are 16-byte aligned (rows of
+// B*W*C elements with W*C a multiple of 8).
+__global__ void copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg) {
+  for (int sidx = blockIdx.y; sidx < nseg; sidx += gridDim.y) {
+    const CopySeg sg = segs[sidx];
+    const long long nv = (long long)(sg.bytes / 16);
+    const uint4* src = reinterpret_cast<const uint4*>(sg.src);
+    uint4* dst = reinterpret_cast<uint4*>(sg.dst);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x)
+      dst[i] = src[i];
+  }
+}
+void launch_copy_segments(const CopySeg* segs_dev, int nseg, unsigned long long max_bytes, cudaStream_t s) {
+  if (nseg <= 0) return;
+  unsigned long long gx = (max_bytes / 16 + 255) / 256;
+  if (gx < 1) gx = 1;
+  if (gx > 296) gx = 296;
+  dim3 grid((unsigned)gx, nseg < 65535 ? nseg : 65535);
+  copy_segments_kernel<<<grid, 256, 0, s>>>(segs_dev, nseg);
+}
+
+void launch_memset_zero(void* p, size_t bytes, cudaStream_t s) { cudaMemsetAsync(p, 0, bytes, s); }
+
+}  // namespace pcpp

@@ -1,0 +1,171 @@
+// SIMT implicit-GEMM conv3x3 / 1x1 (fp32 accumulate).  Used for:
+//  * every contraction in fp32 mode (parity mode, rel-L2 <= 1e-5; no fp32 tensor-core kind exists),
+//  * conv_in (Cin = 4) in both modes, and as the bf16 fallback for shapes the tcgen05 path rejects.
+// Halo rows (r = -1, rows) come from the padded input tensor (filled by the exchange, reading D8);
+// columns outside [0, W) are zero padding.
+#include "../common.cuh"
+#include "../kernels.h"
+
+namespace pcpp {
+
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <typename TA>
+__device__ __forceinline__ float load_a(const GemmArgs& g, int r, int b, int w, bool valid, int k) {
+  if (!valid) return 0.f;
+  int tap = k / g.cin, c = k - tap * g.cin;
+  int dr = 0, dw = 0;
+  if (g.taps == 9) { dr = tap / 3 - 1; dw = tap % 3 - 1; }
+  int ri = r * g.stride + dr, wi = w * g.stride + dw;
+  const ActView& v = (c < g.c0) ? g.a0 : g.a1;
+  if (c >= g.c0) c -= g.c0;
+  if (wi < 0 || wi >= v.W) return 0.f;
+  const TA* p = reinterpret_cast<const TA*>(v.base);
+  return to_f(p[(((long long)ri * v.B + b) * v.W + wi) * v.C + c]);
+}
+
+__device__ __forceinline__ void store_out(const ActView& v, long long idx, float x) {
+  if (v.dtype == DT_F32) reinterpret_cast<float*>(v.base)[idx] = x;
+  else reinterpret_cast<bf16*>(v.base)[idx] = __float2bfloat16_rn(x);
+}
+__device__ __forceinline__ float load_res(const ActView& v, long long idx) {
+  return v.dtype == DT_F32 ? reinterpret_cast<const float*>(v.base)[idx]
+                           : __bfloat162float(reinterpret_cast<const bf16*>(v.base)[idx]);
+}
+}  // namespace
+
+template <typename TA, typename TW>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int M = g.rows_out * g.B * g.w_out;
+  const int K = g.taps * g.cin;
+  // the 4 A rows this thread loads: mm = ty + 16 i
+  int ar[4], ab[4], aw[4]; bool av[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty + 16 * i;
+    av[i] = m < M;
+    int mm = av[i] ? m : 0;
+    aw[i] = mm % g.w_out; int t = mm / g.w_out; ab[i] = t % g.B; ar[i] = t / g.B;
+  }
+  const TW* Wt = reinterpret_cast<const TW*>(g.w);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    const int k = k0 + tx;
+    const bool kv = k < K;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      As[tx][ty + 16 * i] = kv ? load_a<TA>(g, ar[i], ab[i], aw[i], av[i], k) : 0.f;
+      int n = n0 + ty + 16 * i;
+      Bs[tx][ty + 16 * i] = (kv && n < g.N) ? to_f(Wt[(long long)n * K + k]) : 0.f;
+    }
+    __syncthreads();
+    float part[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) part[i][j] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As[kk][ty * 4 + i]; b[i] = Bs[kk][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) part[i][j] = fmaf(a[i], b[j], part[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] += part[i][j];   // blocked summation (fp32-mode accuracy)
+    __syncthreads();
+  }
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+    int w = m % g.w_out; int t = m / g.w_out; int b = t % g.B; int r = t / g.B;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx * 4 + j;
+      if (n >= g.N) continue;
+      float v = acc[i][j];
+      if (g.bias) v += g.bias[n];
+      if (g.temb) v += g.temb[b * g.temb_ld + n];
+      if (n < g.n_split) {
+        long long idx = (((long long)r * g.out.B + b) * g.out.W + w) * g.out.C + n;
+        if (g.res.base) v += load_res(g.res, (((long long)r * g.res.B + b) * g.res.W + w) * g.res.C + n);
+        store_out(g.out, idx, v);
+      } else {
+        int n2 = n - g.n_split;
+        long long idx = (((long long)r * g.out2.B + b) * g.out2.W + w) * g.out2.C + n2;
+        store_out(g.out2, idx, v);
+      }
+    }
+  }
+}
+
+void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
+  const int M = g.rows_out * g.B * g.w_out;
+  dim3 grid((M + BM - 1) / BM, (g.N + BN - 1) / BN);
+  const int ta = g.a0.dtype;
+  if (ta == DT_F32 && g.wdtype == DT_F32) gemm_simt_kernel<float, float><<<grid, 256, 0, s>>>(g);
+  else if (ta == DT_BF16 && g.wdtype == DT_BF16) gemm_simt_kernel<bf16, bf16><<<grid, 256, 0, s>>>(g);
+  else if (ta == DT_F32 && g.wdtype == DT_BF16) gemm_simt_kernel<float, bf16><<<grid, 256, 0, s>>>(g);
+  else gemm_simt_kernel<bf16, float><<<grid, 256, 0, s>>>(g);
+}
+
+// ---------------------------------------------------------------------------------------------
+// conv_out: 3x3, Cin -> 4, one warp per output token; lanes split the 9*Cin reduction.
+// ---------------------------------------------------------------------------------------------
+template <typename TA>
+__global__ void __launch_bounds__(256) conv_out_kernel(const ActView in, const float* __restrict__ w,
+                                                        const float* __restrict__ bias, const ActView out) {
+  const int lane = threadIdx.x & 31;
+  const long long tok = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const long long M = (long long)out.rows * out.B * out.W;
+  if (tok >= M) return;
+  const int wo = tok % out.W; const long long t = tok / out.W; const int b = t % out.B; const int r = t / out.B;
+  const int C = in.C, K = 9 * C;
+  const TA* x = reinterpret_cast<const TA*>(in.base);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int tap = 0; tap < 9; ++tap) {
+    const int ri = r + tap / 3 - 1, wi = wo + tap % 3 - 1;
+    if (wi < 0 || wi >= in.W) continue;
+    const TA* px = x + (((long long)ri * in.B + b) * in.W + wi) * C;
+    for (int c = lane; c < C; c += 32) {
+      const float a = to_f(px[c]);
+#pragma unroll
+      for (int o = 0; o < 4; ++o) acc[o] = fmaf(a, w[o * K + tap * C + c], acc[o]);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < 4; ++o)
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], d);
+  if (lane == 0) {
+    float* po = reinterpret_cast<float*>(out.base) + tok * 4;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) po[o] = acc[o] + bias[o];
+  }
+}
+
+void launch_conv_out(const ActView& in, const float* w, const float* bias, const ActView& out, cudaStream_t s) {
+  const long long M = (long long)out.rows * out.B * out.W;
+  dim3 grid((unsigned)((M + 7) / 8));
+  if (in.dtype == DT_F32) conv_out_kernel<float><<<grid, 256, 0, s>>>(in, w, bias, out);
+  else conv_out_kernel<bf16><<<grid, 256, 0, s>>>(in, w, bias, out);
+}
+
+}  // namespace pcpp

@@ -1,0 +1,531 @@
+// Plan memory layout, weight upload, exchange descriptors and the step executor.
+//
+// Exchange protocol (§3.2, reading D6): every buffer whose rows are sent is double-buffered by
+// step parity q = k mod 2.  At async step k a rank sends its fresh rows of parity q and receives
+// its neighbours' rows into parity q buffers that the SAME layer reads at step k+1 (conv halos go
+// to the 1-q copy of the conv-input tensor, bands to recv_{top,bot}[q], GN sums to mall[q]).
+// Reads at step k use what step k-1 received, so the transfer has a whole step of slack
+// ("issued one step ahead") and nothing waits on it inside the step.  Warm-up (sync) steps
+// exchange this step's data and wait for it ("synchronous AllGather").
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <dlfcn.h>
+#include "runtime.h"
+#include "nccl_api.h"
+
+namespace pcpp {
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { set_error("CUDA %s at %s:%d: %s", #x, __FILE__, __LINE__, cudaGetErrorString(e_)); return PCPP_ERR_CUDA; } } while (0)
+
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (api.handle) return &api;
+  if (tried) { set_error("NCCL could not be loaded"); return nullptr; }
+  tried = true;
+  const char* cands[] = {"libnccl.so.2",
+                         "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+  for (const char* c : cands) { api.handle = dlopen(c, RTLD_NOW | RTLD_GLOBAL); if (api.handle) break; }
+  if (!api.handle) { set_error("dlopen(libnccl.so.2) failed"); return nullptr; }
+#define SYM(f, n) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.handle, n)); if (!api.f) { set_error("missing %s", n); api.handle = nullptr; return nullptr; }
+  SYM(GetUniqueId, "ncclGetUniqueId"); SYM(CommInitRank, "ncclCommInitRank"); SYM(CommDestroy, "ncclCommDestroy");
+  SYM(CommAbort, "ncclCommAbort"); SYM(Send, "ncclSend"); SYM(Recv, "ncclRecv"); SYM(AllGather, "ncclAllGather");
+  SYM(GroupStart, "ncclGroupStart"); SYM(GroupEnd, "ncclGroupEnd"); SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+  return &api;
+}
+
+Plan::~Plan() {
+  for (auto& g : graphs) for (auto& x : g) if (x) cudaGraphExecDestroy(x);
+  if (comm && nccl) nccl->CommDestroy(reinterpret_cast<ncclComm_t>(comm));
+  for (auto& r : rm) if (r.arena) cudaFree(r.arena);
+  for (void* p : gallocs) cudaFree(p);
+  if (segs_dev) cudaFree(segs_dev);
+  cudaEvent_t evs[] = {ev_fork, ev_x, ev_join, ev_t0, ev_t1};
+  for (auto e : evs) if (e) cudaEventDestroy(e);
+  if (s1) cudaStreamDestroy(s1);
+  if (own_s0 && s0) cudaStreamDestroy(s0);
+}
+
+// ---------------------------------------------------------------------------------------------
+// memory layout
+// ---------------------------------------------------------------------------------------------
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+pcpp_status plan_allocate(Plan& P) {
+  size_t off = 0;
+  for (auto& t : P.td) {
+    t.off[0] = off; off = align256(off + t.bytes);
+    if (t.dbl) { t.off[1] = off; off = align256(off + t.bytes); } else t.off[1] = t.off[0];
+  }
+  const size_t mb = (size_t)B_CFG * GN_G * 2 * sizeof(double);
+  for (auto& g : P.gns) {
+    for (int q = 0; q < 2; ++q) { g.off_m[q] = off; off = align256(off + mb); }
+    for (int q = 0; q < 2; ++q) { g.off_mall[q] = off; off = align256(off + mb * P.n); }
+    g.off_part = off; off = align256(off + (size_t)B_CFG * g.nchunk * GN_G * 2 * sizeof(double));
+    g.off_cnt = off; off = align256(off + 16);
+  }
+  const size_t es = dtype_size(P.dtype);
+  size_t gat_level[3] = {0, 0, 0};
+  bool have_level[3] = {false, false, false};
+  for (auto& a : P.attns) {
+    const size_t rowb = (size_t)B_CFG * a.W * 2 * a.C * es;
+    for (int q = 0; q < 2; ++q) {
+      a.off_top[q] = off; off = align256(off + std::max<size_t>(16, (size_t)a.r * rowb));
+      a.off_bot[q] = off; off = align256(off + std::max<size_t>(16, (size_t)a.r * rowb));
+    }
+    const size_t gb = (size_t)a.h * P.n * rowb;
+    if (P.n > 1) {
+      if (P.cfg.scheme == PCPP_SCHEME_FULLMAP) {
+        for (int q = 0; q < 2; ++q) { a.off_gat[q] = off; off = align256(off + gb); }
+      } else {
+        if (!have_level[a.level]) { gat_level[a.level] = off; off = align256(off + gb); have_level[a.level] = true; }
+        a.off_gat[0] = a.off_gat[1] = gat_level[a.level];
+      }
+    }
+  }
+  P.rank_bytes = off;
+  P.rm.resize(P.nr);
+  for (int i = 0; i < P.nr; ++i) {
+    cudaError_t e = cudaMalloc(&P.rm[i].arena, P.rank_bytes);
+    if (e != cudaSuccess) { set_error("cudaMalloc(%zu) for rank arena: %s", P.rank_bytes, cudaGetErrorString(e)); return PCPP_ERR_OOM; }
+    P.rm[i].bytes = P.rank_bytes;
+    CK(cudaMemset(P.rm[i].arena, 0, P.rank_bytes));   // zero halo rows at the image borders
+  }
+  auto galloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(bytes, 256)) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, std::max<size_t>(bytes, 256));
+    P.gallocs.push_back(p); return p;
+  };
+  P.wmat = galloc((size_t)P.wmat_len * es);
+  P.wf32 = (float*)galloc((size_t)P.wf32_len * 4);
+  P.emb = (float*)galloc(2 * P.T * 4); P.hid = (float*)galloc(P.T * 4);
+  P.tproj = (float*)galloc((size_t)2 * P.J * 4); P.cond = (float*)galloc(P.T * 4);
+  P.taus = (int*)galloc(P.S * 4); P.coef = (double*)galloc(P.S * 4 * 8); P.k_dev = (int*)galloc(16);
+  for (void* p : P.gallocs) if (!p) { set_error("cudaMalloc failed for global buffers"); return PCPP_ERR_OOM; }
+  // DDIM schedule (reading D2): scaled_linear betas, 'leading' spacing, offset 1, final ab_prev = ab[0]
+  std::vector<double> ab(1000);
+  {
+    const double b0 = std::sqrt(0.00085), b1 = std::sqrt(0.012);
+    double acc = 1.0;
+    for (int t = 0; t < 1000; ++t) {
+      const double bt = b0 + (b1 - b0) * (double)t / 999.0;
+      acc *= (1.0 - bt * bt);
+      ab[t] = acc;
+    }
+  }
+  std::vector<int> taus(P.S); std::vector<double> coef(4 * P.S);
+  const int ratio = 1000 / P.S;
+  for (int k = 0; k < P.S; ++k) {
+    const int tau = (P.S - 1 - k) * ratio + 1;
+    const int prev = tau - ratio;
+    const double at = ab[tau], ap = prev >= 0 ? ab[prev] : ab[0];
+    taus[k] = tau;
+    coef[4 * k + 0] = std::sqrt(at); coef[4 * k + 1] = std::sqrt(1.0 - at);
+    coef[4 * k + 2] = std::sqrt(ap); coef[4 * k + 3] = std::sqrt(1.0 - ap);
+  }
+  CK(cudaMemcpy(P.taus, taus.data(), P.S * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(P.coef, coef.data(), P.S * 4 * 8, cudaMemcpyHostToDevice));
+  return PCPP_OK;
+}
+
+pcpp_status plan_upload_weights(Plan& P, const float* blob) {
+  const size_t es = dtype_size(P.dtype);
+  std::vector<float> f32((size_t)P.wf32_len, 0.f);
+  std::vector<uint16_t> b16;
+  std::vector<float> m32;
+  if (P.dtype == DT_BF16) b16.assign((size_t)P.wmat_len, 0); else m32.assign((size_t)P.wmat_len, 0.f);
+  for (const auto& u : P.uploads) {
+    const float* src = blob + u.blob_off;
+    if (u.f32) { std::memcpy(&f32[u.off], src, (size_t)u.numel * 4); continue; }
+    if (P.dtype == DT_F32) { std::memcpy(&m32[u.off], src, (size_t)u.numel * 4); continue; }
+    for (long long i = 0; i < u.numel; ++i) {   // round-to-nearest-even to bf16
+      uint32_t x; std::memcpy(&x, &src[i], 4);
+      const uint32_t lsb = (x >> 16) & 1u;
+      b16[u.off + i] = (uint16_t)((x + 0x7FFFu + lsb) >> 16);
+    }
+  }
+  CK(cudaMemcpy(P.wf32, f32.data(), f32.size() * 4, cudaMemcpyHostToDevice));
+  if (P.dtype == DT_BF16) { CK(cudaMemcpy(P.wmat, b16.data(), b16.size() * es, cudaMemcpyHostToDevice)); }
+  else { CK(cudaMemcpy(P.wmat, m32.data(), m32.size() * es, cudaMemcpyHostToDevice)); }
+  return PCPP_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// views
+// ---------------------------------------------------------------------------------------------
+static ActView view(const Plan& P, int vr, int t, int par) {
+  const TDesc& d = P.td[t];
+  ActView v;
+  const size_t rowb = (size_t)B_CFG * d.W * d.C * dtype_size(d.dtype);
+  v.base = P.rm[vr].arena + d.off[d.dbl ? par : 0] + (size_t)d.pad * rowb;
+  v.rows = d.rows; v.B = B_CFG; v.W = d.W; v.C = d.C; v.dtype = d.dtype;
+  return v;
+}
+
+static char* resolve(const Plan& P, int vr, const BufRef& r) {
+  char* base = P.rm[vr].arena;
+  switch (r.kind) {
+    case BK_TENSOR: { const TDesc& d = P.td[r.id]; return base + d.off[d.dbl ? r.par : 0] + r.byte_off; }
+    case BK_TOP: return base + P.attns[r.id].off_top[r.par] + r.byte_off;
+    case BK_BOT: return base + P.attns[r.id].off_bot[r.par] + r.byte_off;
+    case BK_GAT: return base + P.attns[r.id].off_gat[r.par] + r.byte_off;
+    case BK_GNM: return base + P.gns[r.id].off_m[r.par] + r.byte_off;
+    case BK_GNMALL: return base + P.gns[r.id].off_mall[r.par] + r.byte_off;
+  }
+  return nullptr;
+}
+
+// ---------------------------------------------------------------------------------------------
+// exchange descriptors
+// ---------------------------------------------------------------------------------------------
+static BufRef tref(const Plan& P, int t, int par, int row) {
+  const TDesc& d = P.td[t];
+  const long long rowb = (long long)B_CFG * d.W * d.C * dtype_size(d.dtype);
+  return BufRef{BK_TENSOR, t, par, (long long)(row + d.pad) * rowb};
+}
+
+static XGroup make_group(const Plan& P, const Op& op, int sync, int par, std::vector<Xfer>& lb) {
+  XGroup G;
+  const int n = P.n;
+  G.wait = sync;
+  lb.clear();
+  if (op.k == OP_HALO) {
+    const HaloX& hx = P.halos[op.xid];
+    const TDesc& d = P.td[hx.t];
+    const size_t rowb = (size_t)B_CFG * d.W * d.C * dtype_size(d.dtype);
+    const int h = d.rows, pd = sync ? par : 1 - par;
+    G.cls = 1;
+    for (int i = 0; i < n; ++i) {
+      if (i > 0) {   // my top halo <- rank i-1's last row
+        Xfer x{1, i - 1, i, tref(P, hx.t, par, h - 1), tref(P, hx.t, pd, -1), rowb};
+        G.remote.push_back(x); lb.push_back(x);
+        if (sync) { G.local.push_back({1, i, i, tref(P, hx.t, par, -1), tref(P, hx.t, 1 - par, -1), rowb});
+                    lb.push_back({1, i - 1, i, tref(P, hx.t, par, h - 1), tref(P, hx.t, 1 - par, -1), rowb}); }
+      }
+      if (i < n - 1 && hx.stride == 1) {   // my bottom halo <- rank i+1's first row
+        Xfer x{1, i + 1, i, tref(P, hx.t, par, 0), tref(P, hx.t, pd, h), rowb};
+        G.remote.push_back(x); lb.push_back(x);
+        if (sync) { G.local.push_back({1, i, i, tref(P, hx.t, par, h), tref(P, hx.t, 1 - par, h), rowb});
+                    lb.push_back({1, i + 1, i, tref(P, hx.t, par, 0), tref(P, hx.t, 1 - par, h), rowb}); }
+      }
+    }
+  } else if (op.k == OP_GN) {
+    const size_t mb = (size_t)B_CFG * GN_G * 2 * sizeof(double);
+    G.cls = 2; G.allgather = 1;
+    G.ag_send = BufRef{BK_GNM, op.xid, par, 0};
+    G.ag_recv = BufRef{BK_GNMALL, op.xid, par, 0};
+    G.ag_bytes = mb;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        Xfer x{2, j, i, BufRef{BK_GNM, op.xid, par, 0}, BufRef{BK_GNMALL, op.xid, par, (long long)(j * mb)}, mb};
+        if (i != j) G.remote.push_back(x);
+        lb.push_back(x);
+      }
+  } else if (op.k == OP_KVX) {
+    const AttnX& a = P.attns[op.xid];
+    const TDesc& d = P.td[a.kv];
+    const size_t rowb = (size_t)B_CFG * d.W * d.C * dtype_size(d.dtype);
+    const int h = a.h, r = a.r;
+    G.cls = 0;
+    const bool fullmap = P.cfg.scheme == PCPP_SCHEME_FULLMAP;
+    if (!sync && !fullmap) {            // PCPP async: only the p-fraction bands, p2p to i +- 1
+      for (int i = 0; i < n && r > 0; ++i) {
+        if (i > 0) { Xfer x{0, i - 1, i, tref(P, a.kv, par, h - r), BufRef{BK_TOP, op.xid, par, 0}, r * rowb}; G.remote.push_back(x); lb.push_back(x); }
+        if (i < n - 1) { Xfer x{0, i + 1, i, tref(P, a.kv, par, 0), BufRef{BK_BOT, op.xid, par, 0}, r * rowb}; G.remote.push_back(x); lb.push_back(x); }
+      }
+    } else {                            // all-gather of the full map (warm-up, or DistriFusion)
+      const int gp = fullmap ? par : 0;
+      G.allgather = 1;
+      G.ag_send = tref(P, a.kv, par, 0);
+      G.ag_recv = BufRef{BK_GAT, op.xid, gp, 0};
+      G.ag_bytes = (size_t)h * rowb;
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+          Xfer x{0, j, i, tref(P, a.kv, par, 0), BufRef{BK_GAT, op.xid, gp, (long long)((size_t)j * h * rowb)}, (size_t)h * rowb};
+          if (i != j) { G.remote.push_back(x); lb.push_back(x); }
+        }
+      if (!fullmap && r > 0) {          // warm-up seeds the band buffers for step k+1 (unpack)
+        for (int i = 0; i < n; ++i) {
+          if (i > 0) {
+            G.local.push_back({0, i, i, BufRef{BK_GAT, op.xid, 0, (long long)((size_t)(i * h - r) * rowb)}, BufRef{BK_TOP, op.xid, par, 0}, r * rowb});
+            lb.push_back({0, i - 1, i, tref(P, a.kv, par, h - r), BufRef{BK_TOP, op.xid, par, 0}, r * rowb});
+          }
+          if (i < n - 1) {
+            G.local.push_back({0, i, i, BufRef{BK_GAT, op.xid, 0, (long long)((size_t)((i + 1) * h) * rowb)}, BufRef{BK_BOT, op.xid, par, 0}, r * rowb});
+            lb.push_back({0, i + 1, i, tref(P, a.kv, par, 0), BufRef{BK_BOT, op.xid, par, 0}, r * rowb});
+          }
+        }
+      }
+    }
+  }
+  return G;
+}
+
+pcpp_status plan_build_exchanges(Plan& P) {
+  P.op_xord.assign(P.ops.size(), -1);
+  int nx = 0;
+  for (size_t i = 0; i < P.ops.size(); ++i) {
+    const OpK k = P.ops[i].k;
+    if ((k == OP_HALO || k == OP_KVX || k == OP_GN) && P.n > 1) P.op_xord[i] = nx++;
+  }
+  std::vector<CopySeg> host;
+  std::vector<Xfer> lb;
+  for (int sync = 0; sync < 2; ++sync)
+    for (int par = 0; par < 2; ++par) {
+      P.xg[sync][par].assign(nx, XGroup{});
+      P.seg_remote[sync][par].assign(nx, Plan::SegRange{});
+      P.seg_local[sync][par].assign(nx, Plan::SegRange{});
+      for (size_t i = 0; i < P.ops.size(); ++i) {
+        const int xo = P.op_xord[i];
+        if (xo < 0) continue;
+        XGroup G = make_group(P, P.ops[i], sync, par, lb);
+        // loopback: every transfer is a device copy (all ranks' arenas live here)
+        if (P.loopback) {
+          Plan::SegRange sr; sr.first = (int)host.size();
+          for (auto& x : lb) {
+            host.push_back(CopySeg{resolve(P, x.src_rank, x.src), resolve(P, x.dst_rank, x.dst), (unsigned long long)x.bytes});
+            sr.maxb = std::max<unsigned long long>(sr.maxb, x.bytes);
+          }
+          sr.count = (int)host.size() - sr.first;
+          P.seg_remote[sync][par][xo] = sr;
+        } else {
+          Plan::SegRange sr; sr.first = (int)host.size();
+          for (auto& x : G.local) {
+            if (x.dst_rank != P.rank0) continue;
+            host.push_back(CopySeg{resolve(P, 0, x.src), resolve(P, 0, x.dst), (unsigned long long)x.bytes});
+            sr.maxb = std::max<unsigned long long>(sr.maxb, x.bytes);
+          }
+          sr.count = (int)host.size() - sr.first;
+          P.seg_local[sync][par][xo] = sr;
+        }
+        P.xg[sync][par][xo] = std::move(G);
+      }
+    }
+  if (!host.empty()) {
+    CK(cudaMalloc(&P.segs_dev, host.size() * sizeof(CopySeg)));
+    CK(cudaMemcpy(P.segs_dev, host.data(), host.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
+  }
+  return PCPP_OK;
+}
+
+// counted ledger: bytes of all cross-rank transfers of one async / warm-up step
+void compute_ledgers(Plan& P, pcpp_info* info) {
+  std::vector<Xfer> lb;
+  for (int c = 0; c < 3; ++c) { info->bytes_counted_async[c] = 0; info->bytes_counted_warmup[c] = 0; }
+  if (P.n == 1) return;
+  for (const Op& op : P.ops) {
+    if (op.k != OP_HALO && op.k != OP_KVX && op.k != OP_GN) continue;
+    for (int sync = 0; sync < 2; ++sync) {
+      XGroup G = make_group(P, op, sync, 0, lb);
+      for (auto& x : G.remote) (sync ? info->bytes_counted_warmup : info->bytes_counted_async)[x.cls] += (long long)x.bytes;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// NCCL
+// ---------------------------------------------------------------------------------------------
+pcpp_status plan_init_comm(Plan& P) {
+  if (P.loopback || P.n == 1) return PCPP_OK;
+  P.nccl = nccl_api();
+  if (!P.nccl) return PCPP_ERR_NCCL;
+  ncclUniqueId id; std::memcpy(&id, P.cfg.nccl_id, sizeof id);
+  ncclComm_t c = nullptr;
+  ncclResult_t r = P.nccl->CommInitRank(&c, P.n, id, P.cfg.rank);
+  if (r != 0) { set_error("ncclCommInitRank: %s", P.nccl->GetErrorString(r)); return PCPP_ERR_NCCL; }
+  P.comm = c;
+  return PCPP_OK;
+}
+
+#define NK(x) do { ncclResult_t r_ = (x); if (r_ != 0) { set_error("NCCL %s: %s", #x, P.nccl->GetErrorString(r_)); return PCPP_ERR_NCCL; } } while (0)
+
+static pcpp_status exchange(Plan& P, int xo, int sync, int par) {
+  const XGroup& G = P.xg[sync][par][xo];
+  if (P.loopback) {
+    const auto& sr = P.seg_remote[sync][par][xo];
+    launch_copy_segments(P.segs_dev + sr.first, sr.count, sr.maxb, P.s0);
+    P.launches_per_step += sr.count > 0;
+    return PCPP_OK;
+  }
+  ncclComm_t comm = reinterpret_cast<ncclComm_t>(P.comm);
+  const int me = P.rank0;
+  CK(cudaEventRecord(P.ev_x, P.s0));
+  CK(cudaStreamWaitEvent(P.s1, P.ev_x, 0));
+  if (G.allgather) {
+    NK(P.nccl->AllGather(resolve(P, 0, G.ag_send), resolve(P, 0, G.ag_recv), G.ag_bytes, nccl_int8, comm, P.s1));
+  } else {
+    NK(P.nccl->GroupStart());
+    for (const Xfer& x : G.remote) {
+      if (x.src_rank == me) NK(P.nccl->Send(resolve(P, 0, x.src), x.bytes, nccl_int8, x.dst_rank, comm, P.s1));
+      if (x.dst_rank == me) NK(P.nccl->Recv(resolve(P, 0, x.dst), x.bytes, nccl_int8, x.src_rank, comm, P.s1));
+    }
+    NK(P.nccl->GroupEnd());
+  }
+  if (G.wait) {
+    CK(cudaEventRecord(P.ev_x, P.s1));
+    CK(cudaStreamWaitEvent(P.s0, P.ev_x, 0));
+    const auto& sr = P.seg_local[sync][par][xo];
+    launch_copy_segments(P.segs_dev + sr.first, sr.count, sr.maxb, P.s0);
+  }
+  return PCPP_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// the step
+// ---------------------------------------------------------------------------------------------
+void launch_gemm_tc_or_simt(const Plan& P, const GemmArgs& g, cudaStream_t s);
+void launch_attn_tc_or_simt(const Plan& P, const AttnArgs& a, cudaStream_t s);
+
+pcpp_status run_step(Plan& P, float* latent, int sync, int par) {
+  const int n = P.n, nr = P.nr;
+  cudaStream_t s = P.s0;
+  P.launches_per_step = 0;
+  const size_t es = dtype_size(P.dtype);
+  const char* wm = reinterpret_cast<const char*>(P.wmat);
+  for (size_t oi = 0; oi < P.ops.size(); ++oi) {
+    const Op& op = P.ops[oi];
+    const int xo = P.op_xord[oi];
+    switch (op.k) {
+      case OP_TEMB:
+        launch_temb(P.wf32 + P.t_w1, P.wf32 + P.t_b1, P.wf32 + P.t_w2, P.wf32 + P.t_b2, P.cond, P.taus, P.k_dev,
+                    P.T, P.SIN, P.hid, P.emb, s);
+        launch_temb_proj(P.wf32 + P.t_wt, P.wf32 + P.t_bt, P.emb, P.T, P.J, P.tproj, s);
+        P.launches_per_step += 3;
+        break;
+      case OP_PREP: {
+        const int h = P.H / n;
+        for (int vr = 0; vr < nr; ++vr) {
+          const float* lat = latent + (P.loopback ? (size_t)vr * h * P.W * 4 : 0);
+          launch_prep_latent(lat, view(P, vr, op.out, par), s);
+        }
+        P.launches_per_step += nr;
+        break;
+      }
+      case OP_HALO:
+      case OP_KVX:
+        if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
+        break;
+      case OP_CONV:
+      case OP_GEMM:
+        for (int vr = 0; vr < nr; ++vr) {
+          GemmArgs g;
+          g.a0 = view(P, vr, op.in0, par);
+          g.c0 = g.a0.C; g.cin = g.a0.C;
+          if (op.in1 >= 0) { g.a1 = view(P, vr, op.in1, par); g.cin += g.a1.C; }
+          g.taps = op.k == OP_CONV ? 9 : 1;
+          g.stride = op.stride;
+          const ActView o = view(P, vr, op.out, par);
+          g.rows_out = o.rows; g.w_out = o.W; g.B = B_CFG;
+          g.w = op.w_f32 ? (const void*)(P.wf32 + op.w) : (const void*)(wm + (size_t)op.w * es);
+          g.wdtype = op.w_f32 ? DT_F32 : P.dtype;
+          g.N = op.N;
+          g.bias = op.b >= 0 ? P.wf32 + op.b : nullptr;
+          if (op.temb_off >= 0) { g.temb = P.tproj + op.temb_off; g.temb_ld = P.J; }
+          if (op.res >= 0) g.res = view(P, vr, op.res, par);
+          g.out = o;
+          if (op.out2 >= 0) { g.out2 = view(P, vr, op.out2, par); g.n_split = op.n_split; }
+          launch_gemm_tc_or_simt(P, g, s);
+        }
+        P.launches_per_step += nr;
+        break;
+      case OP_GN: {
+        const GnX& gx = P.gns[op.xid];
+        for (int vr = 0; vr < nr; ++vr) {
+          GnStatsArgs a;
+          a.x0 = view(P, vr, op.in0, par); a.c0 = a.x0.C; a.C = gx.C;
+          if (op.in1 >= 0) a.x1 = view(P, vr, op.in1, par);
+          char* base = P.rm[vr].arena;
+          a.partial = reinterpret_cast<double*>(base + gx.off_part);
+          a.counter = reinterpret_cast<unsigned*>(base + gx.off_cnt);
+          a.m_out = reinterpret_cast<double*>(base + gx.off_m[par]);
+          a.nchunk = gx.nchunk;
+          launch_gn_stats(a, s);
+        }
+        if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
+        for (int vr = 0; vr < nr; ++vr) {
+          GnApplyArgs a;
+          a.x0 = view(P, vr, op.in0, par); a.c0 = a.x0.C; a.C = gx.C;
+          if (op.in1 >= 0) a.x1 = view(P, vr, op.in1, par);
+          a.out = view(P, vr, op.out, par);
+          a.gamma = P.wf32 + op.g; a.beta = P.wf32 + op.be; a.silu = op.silu;
+          char* base = P.rm[vr].arena;
+          a.nranks = n; a.count = gx.count;
+          a.m_fresh = reinterpret_cast<const double*>(base + gx.off_m[par]);
+          if (n == 1) a.mode = 0;
+          else if (sync) { a.mode = 1; a.mall = reinterpret_cast<const double*>(base + gx.off_mall[par]); }
+          else {
+            a.mode = 2;
+            a.mall = reinterpret_cast<const double*>(base + gx.off_mall[1 - par]);
+            a.m_prev = reinterpret_cast<const double*>(base + gx.off_m[1 - par]);
+          }
+          launch_gn_apply(a, s);
+        }
+        P.launches_per_step += 2 * nr;
+        break;
+      }
+      case OP_ATTN: {
+        const AttnX& ax = P.attns[op.xid];
+        const TDesc& kvd = P.td[ax.kv];
+        const size_t rowb = (size_t)B_CFG * kvd.W * kvd.C * es;
+        const bool fullmap = P.cfg.scheme == PCPP_SCHEME_FULLMAP;
+        for (int vr = 0; vr < nr; ++vr) {
+          const int i = P.rank0 + vr;
+          char* base = P.rm[vr].arena;
+          AttnArgs a;
+          a.q = view(P, vr, op.in0, par).base;
+          a.h = ax.h; a.B = B_CFG; a.W = ax.W; a.C = ax.C; a.dtype = P.dtype;
+          a.out = view(P, vr, op.out, par).base;
+          const void* local = view(P, vr, op.in1, par).base;
+          int ns = 0;
+          if (n == 1) {
+            a.src[ns++] = AttnSrc{local, ax.h};
+          } else if (sync || fullmap) {
+            const int gp = fullmap ? (sync ? par : 1 - par) : 0;
+            const char* gat = base + ax.off_gat[gp];
+            if (i > 0) a.src[ns++] = AttnSrc{gat, i * ax.h};
+            a.src[ns++] = AttnSrc{local, ax.h};
+            if (i < n - 1) a.src[ns++] = AttnSrc{gat + (size_t)(i + 1) * ax.h * rowb, (n - 1 - i) * ax.h};
+          } else {
+            if (i > 0 && ax.r > 0) a.src[ns++] = AttnSrc{base + ax.off_top[1 - par], ax.r};
+            a.src[ns++] = AttnSrc{local, ax.h};
+            if (i < n - 1 && ax.r > 0) a.src[ns++] = AttnSrc{base + ax.off_bot[1 - par], ax.r};
+          }
+          a.nsrc = ns;
+          launch_attn_tc_or_simt(P, a, s);
+        }
+        P.launches_per_step += nr;
+        break;
+      }
+      case OP_UPS:
+        for (int vr = 0; vr < nr; ++vr) launch_upsample2(view(P, vr, op.in0, par), view(P, vr, op.out, par), s);
+        P.launches_per_step += nr;
+        break;
+      case OP_CONVOUT:
+        for (int vr = 0; vr < nr; ++vr)
+          launch_conv_out(view(P, vr, op.in0, par), P.wf32 + op.w, P.wf32 + op.b, view(P, vr, op.out, par), s);
+        P.launches_per_step += nr;
+        break;
+      case OP_CFGDDIM: {
+        const int h = P.H / n;
+        for (int vr = 0; vr < nr; ++vr) {
+          float* lat = latent + (P.loopback ? (size_t)vr * h * P.W * 4 : 0);
+          launch_cfg_ddim(reinterpret_cast<const float*>(view(P, vr, op.in0, par).base), lat, h, P.W,
+                          P.cfg.guidance_scale, P.coef, P.k_dev, s);
+        }
+        P.launches_per_step += nr;
+        break;
+      }
+      case OP_END:
+        launch_step_end(P.k_dev, s);
+        P.launches_per_step += 1;
+        break;
+    }
+  }
+  CK(cudaGetLastError());
+  return PCPP_OK;
+}
+
+}  // namespace pcpp

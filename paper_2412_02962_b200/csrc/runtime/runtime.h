@@ -1,0 +1,145 @@
+// libpcpp runtime: plan (layer program + memory layout + weights), exchange descriptors,
+// executor (eager or CUDA-graph replay), NCCL / loopback backends.
+#pragma once
+#include <cuda_runtime.h>
+#include <string>
+#include <vector>
+#include <memory>
+#include "../common.cuh"
+#include "../kernels.h"
+#include "../../../include/pcpp.h"
+
+namespace pcpp {
+
+constexpr int GN_G = 32;
+constexpr int B_CFG = 2;
+
+// ---- tensors ------------------------------------------------------------------------------------
+struct TDesc {
+  std::string name;
+  int level = 0, rows = 0, W = 0, C = 0, dtype = 0;
+  int pad = 0;       // 1: rows -1 and `rows` exist (conv halo rows, zero at image borders)
+  int dbl = 0;       // 1: one buffer per step parity (its rows are sent to neighbours)
+  size_t bytes = 0;  // per parity, including halo rows
+  size_t off[2] = {0, 0};   // offsets in the rank arena
+};
+
+// ---- ops ------------------------------------------------------------------------------------------
+enum OpK { OP_TEMB, OP_PREP, OP_HALO, OP_CONV, OP_GEMM, OP_GN, OP_KVX, OP_ATTN, OP_UPS, OP_CONVOUT,
+           OP_CFGDDIM, OP_END };
+
+struct Op {
+  OpK k;
+  int in0 = -1, in1 = -1, out = -1, out2 = -1, res = -1;
+  int stride = 1, taps = 1, silu = 0;
+  int n_split = 1 << 30;
+  long long w = -1;         // element offset into wmat (or wf32 when w_f32)
+  int w_f32 = 0;
+  long long b = -1, g = -1, be = -1;   // element offsets into wf32 (bias, gamma, beta)
+  int temb_off = -1;        // column offset into tproj [2][J]
+  int xid = -1;             // exchange id (halo / gn / attn index)
+  int N = 0;                // output channels for GEMM/CONV
+};
+
+// ---- exchange buffers --------------------------------------------------------------------------
+struct HaloX { int t; int stride; };
+struct GnX   { int C; int rows, W; size_t off_m[2], off_mall[2], off_part, off_cnt; int nchunk; double count; };
+struct AttnX { int kv; int level; int h, W, C; int r; size_t off_top[2], off_bot[2]; size_t off_gat[2]; };
+
+// A symbolic buffer reference, resolved per rank to a device pointer.
+enum BufKind { BK_TENSOR, BK_TOP, BK_BOT, BK_GAT, BK_GNM, BK_GNMALL };
+struct BufRef { int kind; int id; int par; long long byte_off; };
+// One transfer of a step's exchange (global view over all ranks).
+struct Xfer { int cls; int src_rank, dst_rank; BufRef src, dst; size_t bytes; };
+// How a backend should realise one exchange point.
+struct XGroup {
+  int cls = 0;                   // 0 attn, 1 conv, 2 gn
+  int allgather = 0;             // NCCL: one ncclAllGather instead of p2p
+  BufRef ag_send{}, ag_recv{};   // allgather buffers (own rank)
+  size_t ag_bytes = 0;           // per-rank contribution
+  std::vector<Xfer> remote;      // cross-rank data (also the counted ledger)
+  std::vector<Xfer> local;       // post-exchange local copies (dual halo write, band unpack)
+  int wait = 0;                  // consumer needs it this step (sync)
+};
+
+struct NcclApi;   // dlopen'd NCCL entry points
+
+struct RankMem { char* arena = nullptr; size_t bytes = 0; };
+
+struct Plan {
+  // configuration
+  int H = 0, W = 0, C = 0, n = 1, warmup = 1, S = 50;
+  double p = 0.0;
+  pcpp_config cfg{};
+  int dtype = DT_BF16;
+  int levels = 1, C0 = 128, T = 512, SIN = 128;
+  int nr = 1;            // virtual ranks held here (n for loopback, 1 for NCCL)
+  int rank0 = 0;         // global rank of virtual rank 0
+  bool loopback = true;
+  bool use_tc = false;
+
+  // program
+  std::vector<TDesc> td;
+  std::vector<Op> ops;
+  std::vector<HaloX> halos;
+  std::vector<GnX> gns;
+  std::vector<AttnX> attns;
+  int J = 0;             // total temb projection width (sum of ResBlock Cout)
+  // manifest
+  std::vector<std::string> man_name;
+  std::vector<std::vector<long long>> man_shape;
+  std::vector<long long> man_off;
+  size_t blob_len = 0;
+  // weight upload list: (blob_off, numel, to_f32_arena, arena_off)
+  struct Up { long long blob_off, numel; int f32; long long off; };
+  std::vector<Up> uploads;
+  long long wmat_len = 0, wf32_len = 0;
+  // temb parameter offsets (wf32)
+  long long t_w1 = 0, t_b1 = 0, t_w2 = 0, t_b2 = 0, t_wt = 0, t_bt = 0;
+
+  // per-rank memory
+  size_t rank_bytes = 0;
+  std::vector<RankMem> rm;
+  // global memory
+  void* wmat = nullptr;  float* wf32 = nullptr;
+  float* emb = nullptr; float* hid = nullptr; float* tproj = nullptr; float* cond = nullptr;
+  int* taus = nullptr; double* coef = nullptr; int* k_dev = nullptr;
+  std::vector<void*> gallocs;
+
+  // exchange descriptors: [sync][par] per exchange op index
+  std::vector<XGroup> xg[2][2];        // indexed by exchange-op ordinal
+  std::vector<int> op_xord;            // op index -> exchange ordinal (-1 if none)
+  CopySeg* segs_dev = nullptr;         // all loopback/local copy segments
+  struct SegRange { int first = 0, count = 0; unsigned long long maxb = 0; };
+  std::vector<SegRange> seg_remote[2][2], seg_local[2][2];
+
+  // execution state
+  cudaStream_t s0 = nullptr, s1 = nullptr; bool own_s0 = false;
+  cudaEvent_t ev_fork = nullptr, ev_x = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+  cudaGraphExec_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  float* graph_latent = nullptr;
+  int k = 0;
+  bool poisoned = false;
+  int launches_per_step = 0;
+  NcclApi* nccl = nullptr;
+  void* comm = nullptr;   // ncclComm_t
+
+  ~Plan();
+};
+
+// builder / layout (runtime.cpp)
+pcpp_status build_program(Plan& P, int model);
+pcpp_status validate(int H, int W, int C, int n, double p, int w, const pcpp_config* cfg);
+void compute_ledgers(Plan& P, pcpp_info* info);
+pcpp_status plan_allocate(Plan& P);
+pcpp_status plan_upload_weights(Plan& P, const float* blob);
+pcpp_status plan_build_exchanges(Plan& P);
+pcpp_status plan_init_comm(Plan& P);
+pcpp_status run_step(Plan& P, float* latent, int sync, int par);
+int band_rows(double p, int h);
+const char* set_error(const char* fmt, ...);
+
+// kernels init
+void kernels_init();
+
+}  // namespace pcpp

@@ -1,0 +1,85 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/pcpp.h declares,
+its own model manifest equals the oracle's, its host-side plan math (band rows, byte ledger) is
+bit-exact against the oracle's closed forms, and argument validation rejects bad plans."""
+import os
+import re
+
+import pytest
+
+from oracle import ledger, model as M
+from oracle.schedule import band_rows
+from paper_2412_02962_b200 import pcpp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "pcpp.h")).read()
+    declared = set(re.findall(r"PCPP_API\s+[\w\s\*]+?\b(pcpp_\w+)\s*\(", hdr))
+    assert len(declared) >= 19
+    L = pcpp.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert declared == set(pcpp.SYMBOLS)
+
+
+@pytest.mark.parametrize("model", ["tiny", "sdxl"])
+def test_manifest_matches_oracle(model):
+    assert pcpp.manifest(model) == [(n, tuple(s)) for n, s, _ in M.manifest(model)]
+    assert pcpp.pcpp_weights_len(model) == sum(M.init_spec(s, k)[0] for _, s, k in M.manifest(model))
+
+
+@pytest.mark.parametrize("model,H,n,p", [("sdxl", 128, 8, 0.8), ("sdxl", 128, 4, 0.8), ("sdxl", 128, 2, 0.3),
+                                         ("sdxl", 256, 8, 0.8), ("sdxl", 480, 8, 0.8), ("sdxl", 128, 8, 0.0),
+                                         ("sdxl", 128, 8, 0.125), ("sdxl", 128, 8, 0.25), ("sdxl", 128, 8, 0.5),
+                                         ("sdxl", 128, 8, 1.0), ("tiny", 32, 2, 0.25), ("sdxl", 32, 8, 0.3),
+                                         ("sdxl", 128, 1, 0.8)])
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_plan_math_bit_exact(model, H, n, p, precision):
+    es = 2 if precision == "bf16" else 4
+    cfg = pcpp.make_config(model=model, precision=precision)
+    info = pcpp.pcpp_plan_info(H, H, 4, n, p, 1 if n > 1 else 0, cfg)
+    lay = [L for L in ledger.layer_table(model, H, H) if L["kind"] == "attn"]
+    assert info["n_attn"] == len(lay)
+    assert info["attn_h"] == [L["H_l"] // n for L in lay]
+    assert info["attn_r"] == [band_rows(p, L["H_l"] // n) for L in lay]
+    cls = ("attn", "conv", "gn")
+    for key, kind in (("bytes_async", "pcpp_async"), ("bytes_warmup", "warmup"), ("bytes_fullmap", "fullmap_async")):
+        want = ledger.physical_bytes(model, H, H, n, p, es, kind)
+        assert info[key] == [want[c] for c in cls], key
+    want = ledger.physical_bytes(model, H, H, n, p, es, "pcpp_async")
+    assert info["bytes_counted_async"] == [want[c] for c in cls]
+    want = ledger.physical_bytes(model, H, H, n, p, es, "warmup")
+    assert info["bytes_counted_warmup"] == [want[c] for c in cls]
+
+
+def test_fullmap_counted_ledger():
+    cfg = pcpp.make_config(model="sdxl", scheme="fullmap")
+    info = pcpp.pcpp_plan_info(128, 128, 4, 8, 0.8, 4, cfg)
+    want = ledger.physical_bytes("sdxl", 128, 128, 8, 0.8, 2, "fullmap_async")
+    assert info["bytes_counted_async"] == [want[c] for c in ("attn", "conv", "gn")]
+
+
+@pytest.mark.parametrize("args", [
+    dict(H=128, n=3, p=0.5, w=1),        # H % 4n
+    dict(H=128, n=16, p=0.5, w=1),       # n > 8
+    dict(H=128, n=8, p=1.5, w=1),        # p > 1 undefined
+    dict(H=128, n=8, p=-0.1, w=1),
+    dict(H=128, n=8, p=0.5, w=0),        # warm-up required for n > 1 (D20)
+    dict(H=128, n=8, p=0.5, w=60),       # w > S
+    dict(H=130, n=1, p=0.5, w=1),
+])
+def test_validation_rejects(args):
+    cfg = pcpp.make_config(model="sdxl")
+    with pytest.raises(pcpp.PcppError) as e:
+        pcpp.pcpp_plan_info(args["H"], 128, 4, args["n"], args["p"], args["w"], cfg)
+    assert e.value.status == pcpp.ERR_INVALID
+
+
+def test_validation_channels_and_nccl_world():
+    cfg = pcpp.make_config(model="sdxl")
+    with pytest.raises(pcpp.PcppError):
+        pcpp.pcpp_plan_info(128, 128, 3, 2, 0.5, 1, cfg)
+    cfg = pcpp.make_config(model="sdxl", backend="nccl", world=4)
+    with pytest.raises(pcpp.PcppError):
+        pcpp.pcpp_plan_info(128, 128, 4, 2, 0.5, 1, cfg)

@@ -1,0 +1,146 @@
+"""Kernel-level parity through the C ABI (pcpp_op_*) against the oracle's ops, at sizes that span
+several tiles and a ragged tail, in fp32 (rel-L2 <= 1e-5) and bf16 (<= 2e-2); pack is bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import model as M
+from oracle.schedule import cfg_combine, ddim_step
+from paper_2412_02962_b200 import inputs, pcpp
+
+pytestmark = pytest.mark.gpu
+TOL = {"fp32": 1e-5, "bf16": 2e-2}
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def T(x, dtype):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    return t.to(torch.bfloat16) if dtype == "bf16" else t
+
+
+def back(t):
+    import torch
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def q(x, dtype):
+    return inputs.round_to_bf16(np.asarray(x, np.float32)).astype(np.float64) if dtype == "bf16" else np.asarray(x, np.float64)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("impl", ["simt", "auto"])
+@pytest.mark.parametrize("shape", [(3, 20, 64, 96, 1), (4, 16, 320, 320, 1), (2, 40, 128, 200, 1),
+                                   (4, 16, 64, 64, 2), (1, 8, 128, 64, 1)])
+def test_conv3x3_with_halo_rows(cuda_ok, dtype, impl, shape):
+    import torch
+    rows, W, Cin, Cout, stride = shape
+    rng = np.random.default_rng(7)
+    x = q(rng.standard_normal((rows + 2, 2, W, Cin)), dtype)           # row 0 / rows+1 are halos
+    w = q(rng.standard_normal((Cout, 3, 3, Cin)) / np.sqrt(9 * Cin), dtype)
+    bias = rng.standard_normal(Cout).astype(np.float32)
+    temb = rng.standard_normal((2, Cout)).astype(np.float32)
+    res = q(rng.standard_normal((rows // stride, 2, W // stride, Cout)), dtype)
+    y = torch.empty((rows // stride, 2, W // stride, Cout), device="cuda",
+                    dtype=torch.float32 if dtype == "fp32" else torch.bfloat16)
+    pcpp.pcpp_op_conv(T(x, dtype), rows, 2, W, Cin, 9, stride, T(w, dtype), T(bias, "fp32"), T(temb, "fp32"),
+                      T(res, dtype), y, Cout, impl=impl)
+    torch.cuda.synchronize()
+    # oracle: 3 ranks, sync mode; the middle rank's patch is x[1:-1], neighbours supply the halos
+    xb = np.transpose(x, (1, 0, 2, 3))                                   # [B, rows+2, W, C]
+    top = np.zeros((2, rows, W, Cin)); top[:, -1] = xb[:, 0]
+    bot = np.zeros((2, rows, W, Cin)); bot[:, 0] = xb[:, -1]
+    ctx = M.Ctx(3, 0.0, "sync")
+    ref = M.conv3x3(ctx, [top, xb[:, 1:-1], bot], w, bias.astype(np.float64), stride)[1]
+    ref = ref + temb.astype(np.float64)[:, None, None, :] + np.transpose(res, (1, 0, 2, 3))
+    got = np.transpose(back(y), (1, 0, 2, 3))
+    assert rel(got, ref) <= TOL[dtype] / (10 if dtype == "fp32" else 2)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("impl", ["simt", "auto"])
+def test_gemm_1x1_split_free(cuda_ok, dtype, impl):
+    import torch
+    rng = np.random.default_rng(3)
+    rows, W, Cin, Cout = 5, 48, 640, 384
+    x = q(rng.standard_normal((rows, 2, W, Cin)), dtype)
+    w = q(rng.standard_normal((Cout, Cin)) / np.sqrt(Cin), dtype)
+    bias = rng.standard_normal(Cout).astype(np.float32)
+    y = torch.empty((rows, 2, W, Cout), device="cuda", dtype=torch.float32 if dtype == "fp32" else torch.bfloat16)
+    pcpp.pcpp_op_conv(T(x, dtype), rows, 2, W, Cin, 1, 1, T(w, dtype), T(bias, "fp32"), None, None, y, Cout, impl=impl)
+    torch.cuda.synchronize()
+    ref = x @ w.T + bias
+    assert rel(back(y), ref) <= TOL[dtype] / (10 if dtype == "fp32" else 2)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("impl", ["simt", "auto"])
+@pytest.mark.parametrize("geo", [(4, 32, 640, (3, 4, 3)), (8, 64, 128, (0, 8, 6)), (3, 40, 128, (2, 3, 0)),
+                                 (16, 16, 1280, (4, 16, 4)), (2, 120, 64, (1, 2, 1))])
+def test_attention_sources(cuda_ok, dtype, impl, geo):
+    import torch
+    h, W, Cm, rows = geo
+    rng = np.random.default_rng(11)
+    qx = q(rng.standard_normal((h, 2, W, Cm)), dtype)
+    srcs = [q(rng.standard_normal((r, 2, W, 2 * Cm)), dtype) for r in rows if r > 0]
+    kv_rows = [r for r in rows if r > 0]
+    out = torch.empty((h, 2, W, Cm), device="cuda", dtype=torch.float32 if dtype == "fp32" else torch.bfloat16)
+    kvs = [T(s, dtype) for s in srcs]
+    pcpp.pcpp_op_attention(T(qx, dtype), kvs, kv_rows, h, 2, W, Cm, out, impl=impl)
+    torch.cuda.synchronize()
+    K = np.concatenate([s[..., :Cm] for s in srcs], axis=0)              # [rows_ctx, B, W, C]
+    V = np.concatenate([s[..., Cm:] for s in srcs], axis=0)
+    ref = np.zeros((h, 2, W, Cm))
+    for b in range(2):
+        Qb = qx[:, b].reshape(-1, Cm); Kb = K[:, b].reshape(-1, Cm); Vb = V[:, b].reshape(-1, Cm)
+        for hd in range(Cm // 64):
+            sl = slice(hd * 64, hd * 64 + 64)
+            Pm = M._softmax_rows(Qb[:, sl] @ Kb[:, sl].T / 8.0)
+            ref[:, b, :, sl] = (Pm @ Vb[:, sl]).reshape(h, W, 64)
+    assert rel(back(out), ref) <= TOL[dtype] / (10 if dtype == "fp32" else 2)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("shape", [(16, 32, 320), (3, 24, 640), (64, 64, 128), (2, 32, 2560)])
+def test_groupnorm(cuda_ok, dtype, shape):
+    import torch
+    rows, W, Cm = shape
+    rng = np.random.default_rng(5)
+    x = q(rng.standard_normal((rows, 2, W, Cm)) * 2 + 0.5, dtype)
+    g = (1 + 0.1 * rng.standard_normal(Cm)).astype(np.float32)
+    be = (0.1 * rng.standard_normal(Cm)).astype(np.float32)
+    y = torch.empty((rows, 2, W, Cm), device="cuda", dtype=torch.float32 if dtype == "fp32" else torch.bfloat16)
+    m = torch.empty((2, 32, 2), device="cuda", dtype=torch.float64)
+    pcpp.pcpp_op_groupnorm(T(x, dtype), rows, 2, W, Cm, T(g, "fp32"), T(be, "fp32"), 1, y, m)
+    torch.cuda.synchronize()
+    ctx = M.Ctx(1, 0.0, "sync")
+    ref = M.group_norm(ctx, [np.transpose(x, (1, 0, 2, 3))], g.astype(np.float64), be.astype(np.float64), True)[0]
+    assert rel(np.transpose(back(y), (1, 0, 2, 3)), ref) <= TOL[dtype] / (10 if dtype == "fp32" else 2)
+    np.testing.assert_allclose(m.cpu().numpy(), ctx.nxt[("gn0", "m")][0], rtol=1e-6)
+
+
+def test_pack_rows_bit_exact(cuda_ok):
+    import torch
+    src = torch.randint(0, 255, (12, 2, 32, 2 * 640), dtype=torch.uint8, device="cuda").view(torch.bfloat16)
+    rowb = src[0].numel() * 2
+    dst = torch.empty_like(src[:5])
+    pcpp.pcpp_op_pack_rows(src, rowb, 7, 5, dst)
+    torch.cuda.synchronize()
+    assert torch.equal(dst.view(torch.uint8), src[7:12].contiguous().view(torch.uint8))
+
+
+@pytest.mark.parametrize("k", [0, 17, 49])
+def test_cfg_ddim(cuda_ok, k):
+    import torch
+    rng = np.random.default_rng(k)
+    h, W = 24, 40
+    eps = rng.standard_normal((h, 2, W, 4)).astype(np.float32)
+    x = rng.standard_normal((h, W, 4)).astype(np.float32)
+    xt = T(x, "fp32")
+    pcpp.pcpp_op_cfg_ddim(T(eps, "fp32"), xt, h, W, 5.0, 50, k)
+    torch.cuda.synchronize()
+    e = cfg_combine(eps[:, 0].astype(np.float64), eps[:, 1].astype(np.float64), 5.0)
+    ref = ddim_step(x.astype(np.float64), e, 50, k)
+    assert rel(back(xt), ref) <= 1e-6

@@ -1,0 +1,123 @@
+"""Whole-path parity: libpcpp (through the C ABI, loopback backend = n virtual ranks on one GPU)
+against the fp64 oracle on the same seeded inputs.  Tolerances (north star / SURVEY §8(c)):
+rel-L2 <= 1e-5 in fp32 mode and <= 2e-2 in bf16 mode, per step and on the final latent."""
+import functools
+
+import numpy as np
+import pytest
+
+from oracle import model as M
+from oracle import pcpp as OP
+from paper_2412_02962_b200 import inputs, pcpp
+from tests import _data
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-5, "bf16": 2e-2}
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+@functools.lru_cache(maxsize=None)
+def weights(model, precision):
+    b = _data.blob(model)
+    return inputs.round_to_bf16(b) if precision == "bf16" else b
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_run(model, H, n, p, w, S, precision, scheme, max_steps):
+    cfg = OP.Config(model=model, H=H, W=H, n=n, p=p, warmup=w, steps=S, scheme=scheme)
+    out = OP.sample(cfg, weights(model, precision), _data.latent(H, H), _data.cond(model), max_steps=max_steps)
+    return out["xs"]
+
+
+def lib_run(model, H, n, p, w, S, precision, scheme, max_steps, kernels="auto", graphs=True):
+    import torch
+    cfg = pcpp.make_config(model=model, num_steps=S, precision=precision, scheme=scheme, kernels=kernels,
+                           graphs=graphs)
+    plan = pcpp.Plan(H, H, 4, n, p, w, cfg, weights(model, precision))
+    plan.pcpp_set_cond(_data.cond(model))
+    lat = torch.from_numpy(np.array(_data.latent(H, H))).cuda()
+    xs = []
+    for k in range(max_steps):
+        plan.pcpp_step(lat, k)
+        torch.cuda.synchronize()
+        xs.append(lat.cpu().numpy().copy())
+    info = plan.pcpp_query()
+    plan.close()
+    return xs, info
+
+
+CASES = [
+    # model, H, n, p, w, S, precision, scheme, max_steps
+    ("tiny", 32, 2, 0.25, 1, 4, "fp32", "pcpp", 4),      # config T
+    ("tiny", 32, 2, 0.25, 1, 4, "bf16", "pcpp", 4),
+    ("tiny", 32, 1, 0.25, 0, 4, "fp32", "pcpp", 4),
+    ("tiny", 32, 4, 0.5, 1, 4, "fp32", "pcpp", 4),
+    ("tiny", 32, 4, 0.0, 1, 4, "fp32", "pcpp", 3),
+    ("tiny", 32, 4, 0.5, 2, 4, "fp32", "fullmap", 4),
+    ("tiny", 32, 2, 1.0, 1, 4, "fp32", "sync", 3),
+    ("tiny", 32, 8, 1.0, 1, 4, "bf16", "pcpp", 3),
+    ("sdxl", 32, 2, 0.3, 1, 50, "fp32", "pcpp", 2),
+    ("sdxl", 32, 8, 0.8, 1, 50, "bf16", "pcpp", 2),
+    ("sdxl", 32, 1, 0.0, 0, 50, "bf16", "pcpp", 2),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c)))
+def test_path_matches_oracle(cuda_ok, case):
+    model, H, n, p, w, S, precision, scheme, ms = case
+    ref = oracle_run(*case)
+    got, info = lib_run(*case)
+    errs = [rel_l2(g, r) for g, r in zip(got, ref)]
+    print(case, "rel-L2 per step:", ["%.2e" % e for e in errs], "tc:", info["tc_kernels"])
+    assert all(e <= TOL[precision] for e in errs), errs
+
+
+def test_bf16_simt_and_tc_agree_with_oracle(cuda_ok):
+    case = ("tiny", 32, 2, 0.25, 1, 4, "bf16", "pcpp", 4)
+    ref = oracle_run(*case)
+    for kern in ("simt", "auto"):
+        got, _ = lib_run(*case, kernels=kern)
+        errs = [rel_l2(g, r) for g, r in zip(got, ref)]
+        assert all(e <= TOL["bf16"] for e in errs), (kern, errs)
+
+
+def test_graph_replay_equals_eager_bitwise(cuda_ok):
+    case = ("tiny", 32, 4, 0.5, 1, 4, "bf16", "pcpp", 4)
+    a, _ = lib_run(*case, graphs=True)
+    b, _ = lib_run(*case, graphs=False)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_step_protocol_errors(cuda_ok):
+    import torch
+    cfg = pcpp.make_config(model="tiny", num_steps=4, precision="bf16")
+    plan = pcpp.Plan(32, 32, 4, 2, 0.25, 1, cfg, weights("tiny", "bf16"))
+    plan.pcpp_set_cond(_data.cond("tiny"))
+    lat = torch.zeros(32, 32, 4, device="cuda")
+    with pytest.raises(pcpp.PcppError) as e:
+        plan.pcpp_step(lat, 1)                   # must start at k = 0
+    assert e.value.status == pcpp.ERR_STATE
+    for k in range(4):
+        plan.pcpp_step(lat, k)
+    with pytest.raises(pcpp.PcppError):
+        plan.pcpp_step(lat, 4)                   # past the last step
+    plan.pcpp_reset()
+    plan.pcpp_step(lat, 0)
+    torch.cuda.synchronize()
+    plan.close()
+
+
+def test_sample_e2e_host_buffers(cuda_ok):
+    case = ("tiny", 32, 2, 0.25, 1, 4, "bf16", "pcpp", 4)
+    cfg = pcpp.make_config(model="tiny", num_steps=4, precision="bf16")
+    plan = pcpp.Plan(32, 32, 4, 2, 0.25, 1, cfg, weights("tiny", "bf16"))
+    x0 = plan.pcpp_sample(np.array(_data.latent(32, 32)), np.array(_data.cond("tiny")))
+    x0b = plan.pcpp_sample(np.array(_data.latent(32, 32)), np.array(_data.cond("tiny")))
+    plan.close()
+    np.testing.assert_array_equal(x0, x0b)       # deterministic, reset works
+    assert rel_l2(x0, oracle_run(*case)[-1]) <= TOL["bf16"]
