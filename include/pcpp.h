@@ -93,6 +93,9 @@ typedef struct {
   int n_kernels_per_step;               /* kernel launches per step (all virtual ranks) */
   int graphs;                           /* 1 if steps replay CUDA graphs */
   int tc_kernels;                       /* 1 if the tcgen05 contraction kernels are in use */
+  double step_flops;                    /* algorithmic flops of one async step (conv/GEMM 2MNK + attention
+                                           4 q kv C B), summed over the ranks this plan holds */
+  double step_flops_rank_max;           /* the same for the busiest single rank (interior) */
 } pcpp_info;
 
 /* ---- setup ------------------------------------------------------------------------------- */
@@ -148,6 +151,16 @@ PCPP_API pcpp_status pcpp_sample(pcpp_plan_t plan, const float* xT_host, const f
 PCPP_API pcpp_status pcpp_reset(pcpp_plan_t plan);
 
 PCPP_API pcpp_status pcpp_query(pcpp_plan_t plan, pcpp_info* out);
+
+/* Per-kind device time of one step, measured in isolation: the ops of `kind_mask` (1 conv/GEMM,
+ * 2 attention, 4 GroupNorm, 8 exchanges, 16 other elementwise) of a step of type `sync` are captured
+ * alone into a CUDA graph and replayed `iters` times between CUDA events on the plan's stream
+ * (after one untimed replay).  Reports the mean ms per step and the algorithmic work of those ops
+ * (flops = 2MNK for contractions, 4 q kv C B for attention; bytes = HBM bytes for GroupNorm,
+ * exchanged bytes for exchanges).  Does not advance the step counter; buffer contents are left
+ * stale -- call pcpp_reset before the next sample.  latent: as for pcpp_step. */
+typedef struct { double ms; double flops; double bytes; int launches; } pcpp_prof;
+PCPP_API pcpp_status pcpp_profile(pcpp_plan_t plan, float* latent, int kind_mask, int sync, int iters, pcpp_prof* out);
 PCPP_API void pcpp_destroy(pcpp_plan_t plan);
 PCPP_API const char* pcpp_last_error(void);
 

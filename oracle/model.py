@@ -186,6 +186,10 @@ def weight_specs(model: str):
     return [init_spec(shape, kind) for _, shape, kind in manifest(model)]
 
 
+# (The same rule, derived from names/shapes only, lives in paper_2412_02962_b200/inputs.py
+#  for callers that hold the library's manifest; tests/test_abi.py checks the two agree.)
+
+
 class Params:
     """Name -> float64 array view over the flat blob (manifest order)."""
 

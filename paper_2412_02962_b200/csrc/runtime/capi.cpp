@@ -123,6 +123,16 @@ static void fill_info(Plan& P, pcpp_info* info) {
     }
   }
   info->n_kernels_per_step = (int)nk;
+  double fl = 0, by = 0; int nl = 0;
+  op_work(P, K_GEMM | K_ATTN, 0, &fl, &by, &nl);
+  info->step_flops = fl;
+  // busiest rank: an interior rank (or rank 0 when n <= 2)
+  Plan& Q = P;
+  const int sv_nr = Q.nr, sv_r0 = Q.rank0;
+  Q.nr = 1; Q.rank0 = P.n > 2 ? 1 : 0;
+  op_work(Q, K_GEMM | K_ATTN, 0, &fl, &by, &nl);
+  Q.nr = sv_nr; Q.rank0 = sv_r0;
+  info->step_flops_rank_max = fl;
 }
 
 static pcpp_status setup_plan(Plan& P, int H, int W, int C, int n, double p, int w, const pcpp_config* cfg) {
@@ -298,6 +308,43 @@ pcpp_status pcpp_query(pcpp_plan_t h, pcpp_info* info) {
   info->device_bytes = (long long)P.rank_bytes * P.nr + (long long)P.wmat_len * (long long)dtype_size(P.dtype) + P.wf32_len * 4;
   info->graphs = P.cfg.use_graphs;
   info->tc_kernels = P.use_tc;
+  return PCPP_OK;
+  GUARD_END
+}
+
+pcpp_status pcpp_profile(pcpp_plan_t h, float* latent, int kind, int sync, int iters, pcpp_prof* out) {
+  GUARD_BEGIN
+  if (!h || !latent || !out || iters < 1 || kind <= 0 || (kind & ~31)) { set_error("pcpp_profile: bad arguments"); return PCPP_ERR_INVALID; }
+  Plan& P = *h->P;
+  if (P.poisoned) { set_error("plan is poisoned"); return PCPP_ERR_STATE; }
+  sync = (P.n > 1 && sync) ? 1 : 0;
+  const bool fork = !P.loopback && P.n > 1;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  CKS(cudaStreamSynchronize(P.s0));
+  CKS(cudaStreamBeginCapture(P.s0, cudaStreamCaptureModeRelaxed));
+  if (fork) { cudaEventRecord(P.ev_fork, P.s0); cudaStreamWaitEvent(P.s1, P.ev_fork, 0); }
+  pcpp_status st = run_step(P, latent, sync, P.k & 1, (unsigned)kind);
+  if (fork) { cudaEventRecord(P.ev_join, P.s1); cudaStreamWaitEvent(P.s0, P.ev_join, 0); }
+  cudaError_t e = cudaStreamEndCapture(P.s0, &g);
+  if (st != PCPP_OK) { if (g) cudaGraphDestroy(g); return st; }
+  CKS(e);
+  CKS(cudaGraphInstantiate(&ge, g, 0));
+  cudaGraphDestroy(g);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  cudaGraphLaunch(ge, P.s0);
+  cudaEventRecord(a, P.s0);
+  for (int i = 0; i < iters; ++i) cudaGraphLaunch(ge, P.s0);
+  cudaEventRecord(b, P.s0);
+  e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a); cudaEventDestroy(b);
+  cudaGraphExecDestroy(ge);
+  CKS(e);
+  out->ms = ms / iters;
+  op_work(P, (unsigned)kind, sync, &out->flops, &out->bytes, &out->launches);
   return PCPP_OK;
   GUARD_END
 }

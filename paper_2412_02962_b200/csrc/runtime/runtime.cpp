@@ -379,7 +379,18 @@ static pcpp_status exchange(Plan& P, int xo, int sync, int par) {
 void launch_gemm_tc_or_simt(const Plan& P, const GemmArgs& g, cudaStream_t s);
 void launch_attn_tc_or_simt(const Plan& P, const AttnArgs& a, cudaStream_t s);
 
-pcpp_status run_step(Plan& P, float* latent, int sync, int par) {
+static unsigned op_kind(OpK k) {
+  switch (k) {
+    case OP_CONV: case OP_GEMM: return K_GEMM;
+    case OP_ATTN: return K_ATTN;
+    case OP_GN: return K_GN;
+    case OP_HALO: case OP_KVX: return K_XCH;
+    case OP_END: return K_END;
+    default: return K_MISC;
+  }
+}
+
+pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
   const int n = P.n, nr = P.nr;
   cudaStream_t s = P.s0;
   P.launches_per_step = 0;
@@ -387,7 +398,12 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par) {
   const char* wm = reinterpret_cast<const char*>(P.wmat);
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
     const Op& op = P.ops[oi];
-    const int xo = P.op_xord[oi];
+    const int xo_all = P.op_xord[oi];
+    const unsigned kind = op_kind(op.k);
+    if (!(mask & kind) && !(op.k == OP_GN && (mask & K_XCH))) continue;
+    const int xo = (mask & K_XCH) ? xo_all : -1;
+    const bool do_op = (mask & kind) != 0;
+    if (!do_op && op.k != OP_GN) continue;
     switch (op.k) {
       case OP_TEMB:
         launch_temb(P.wf32 + P.t_w1, P.wf32 + P.t_b1, P.wf32 + P.t_w2, P.wf32 + P.t_b2, P.cond, P.taus, P.k_dev,
@@ -433,7 +449,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par) {
         break;
       case OP_GN: {
         const GnX& gx = P.gns[op.xid];
-        for (int vr = 0; vr < nr; ++vr) {
+        for (int vr = 0; vr < nr && do_op; ++vr) {
           GnStatsArgs a;
           a.x0 = view(P, vr, op.in0, par); a.c0 = a.x0.C; a.C = gx.C;
           if (op.in1 >= 0) a.x1 = view(P, vr, op.in1, par);
@@ -445,7 +461,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par) {
           launch_gn_stats(a, s);
         }
         if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
-        for (int vr = 0; vr < nr; ++vr) {
+        for (int vr = 0; vr < nr && do_op; ++vr) {
           GnApplyArgs a;
           a.x0 = view(P, vr, op.in0, par); a.c0 = a.x0.C; a.C = gx.C;
           if (op.in1 >= 0) a.x1 = view(P, vr, op.in1, par);
@@ -526,6 +542,57 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par) {
   }
   CK(cudaGetLastError());
   return PCPP_OK;
+}
+
+void op_work(const Plan& P, unsigned kind, int sync, double* flops, double* bytes, int* launches) {
+  double f = 0, by = 0; int nl = 0;
+  const int n = P.n;
+  const double es = (double)dtype_size(P.dtype);
+  for (size_t oi = 0; oi < P.ops.size(); ++oi) {
+    const Op& op = P.ops[oi];
+    if (!(op_kind(op.k) & kind)) continue;
+    switch (op.k) {
+      case OP_CONV: case OP_GEMM: {
+        const TDesc& o = P.td[op.out];
+        double cin = P.td[op.in0].C + (op.in1 >= 0 ? P.td[op.in1].C : 0);
+        const double M = (double)o.rows * B_CFG * o.W;
+        f += 2.0 * M * op.N * (op.k == OP_CONV ? 9 : 1) * cin * P.nr;
+        nl += P.nr;
+        break;
+      }
+      case OP_ATTN: {
+        const AttnX& a = P.attns[op.xid];
+        for (int vr = 0; vr < P.nr; ++vr) {
+          const int i = P.rank0 + vr;
+          int kv = a.h;
+          if (n > 1) {
+            if (sync || P.cfg.scheme == PCPP_SCHEME_FULLMAP) kv = a.h * n;
+            else kv = a.h + (i > 0 ? a.r : 0) + (i < n - 1 ? a.r : 0);
+          }
+          f += 4.0 * ((double)a.h * a.W) * ((double)kv * a.W) * a.C * B_CFG;
+          by += ((double)a.h * a.W * a.C * 2 + (double)kv * a.W * 2 * a.C) * B_CFG * es;   // Q + O + K/V
+        }
+        nl += P.nr;
+        break;
+      }
+      case OP_GN: {
+        const TDesc& x = P.td[op.in0];
+        double C = x.C + (op.in1 >= 0 ? P.td[op.in1].C : 0);
+        by += 3.0 * x.rows * B_CFG * x.W * C * es * P.nr;     // stats read + apply read/write
+        nl += 2 * P.nr;
+        break;
+      }
+      default:
+        nl += 1;
+        break;
+    }
+  }
+  if (kind & K_XCH) {
+    pcpp_info info;
+    compute_ledgers(const_cast<Plan&>(P), &info);
+    for (int c = 0; c < 3; ++c) by += (double)(sync ? info.bytes_counted_warmup[c] : info.bytes_counted_async[c]);
+  }
+  *flops = f; *bytes = by; *launches = nl;
 }
 
 }  // namespace pcpp

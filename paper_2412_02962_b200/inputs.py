@@ -24,6 +24,43 @@ SEED_XT = 1
 SEED_COND = 2
 
 
+def init_specs(manifest) -> list[tuple[int, float, float]]:
+    """(numel, mean, std) per manifest entry [(name, shape), ...] -- reading D17.
+
+    conv [Cout,3,3,Cin]: std 1/sqrt(9 Cin) (x 1/sqrt(2) for a ResBlock's conv2);
+    linear [out,in]: std 1/sqrt(in) (x 1/sqrt(2 depth) for W_o of an attention stack of that
+    depth, x 1/sqrt(2) for proj_out); GN gamma 1 + 0.1 z, GN beta / biases 0.1 z.
+    The rule reads only names and shapes, so both sides can derive it from their own manifest.
+    """
+    names = [n for n, _ in manifest]
+    depth = {}
+    for n in names:
+        if n.endswith(".wo"):
+            pre = n[: n.rindex(".attn")]
+            depth[pre] = depth.get(pre, 0) + 1
+    out = []
+    for name, shape in manifest:
+        numel = int(np.prod(shape))
+        leaf = name.rsplit(".", 1)[-1]
+        if len(shape) == 4:
+            std = 1.0 / np.sqrt(9 * shape[3])
+            if name.endswith(".conv2.w"):
+                std /= np.sqrt(2.0)
+            out.append((numel, 0.0, float(std)))
+        elif len(shape) == 2:
+            std = 1.0 / np.sqrt(shape[1])
+            if leaf == "wo":
+                std /= np.sqrt(2.0 * depth[name[: name.rindex(".attn")]])
+            elif name.endswith("proj_out.w"):
+                std /= np.sqrt(2.0)
+            out.append((numel, 0.0, float(std)))
+        elif leaf == "g":
+            out.append((numel, 1.0, 0.1))
+        else:                                   # GN beta ('.b' of a norm) and every bias
+            out.append((numel, 0.0, 0.1))
+    return out
+
+
 def make_weight_blob(specs, seed: int = SEED_WEIGHTS) -> np.ndarray:
     """specs: iterable of (numel, mean, std).  Returns one flat float32 blob.
 

@@ -37,7 +37,7 @@ class pcpp_info(C.Structure):
                 ("bytes_fullmap", C.c_longlong * 3), ("bytes_counted_async", C.c_longlong * 3),
                 ("bytes_counted_warmup", C.c_longlong * 3), ("last_step_ms", C.c_double),
                 ("device_bytes", C.c_longlong), ("n_kernels_per_step", C.c_int), ("graphs", C.c_int),
-                ("tc_kernels", C.c_int)]
+                ("tc_kernels", C.c_int), ("step_flops", C.c_double), ("step_flops_rank_max", C.c_double)]
 
     def as_dict(self):
         d = {}
@@ -51,7 +51,11 @@ class pcpp_info(C.Structure):
         return d
 
 
-SYMBOLS = ["pcpp_config_default", "pcpp_get_unique_id", "pcpp_weights_len", "pcpp_manifest_count",
+class pcpp_prof(C.Structure):
+    _fields_ = [("ms", C.c_double), ("flops", C.c_double), ("bytes", C.c_double), ("launches", C.c_int)]
+
+
+SYMBOLS = ["pcpp_profile", "pcpp_config_default", "pcpp_get_unique_id", "pcpp_weights_len", "pcpp_manifest_count",
            "pcpp_manifest_entry", "pcpp_plan", "pcpp_plan_info", "pcpp_set_cond", "pcpp_step",
            "pcpp_sample", "pcpp_reset", "pcpp_query", "pcpp_destroy", "pcpp_last_error",
            "pcpp_op_conv", "pcpp_op_attention", "pcpp_op_groupnorm", "pcpp_op_pack_rows",
@@ -82,6 +86,7 @@ def lib():
     L.pcpp_reset.argtypes = [P]; L.pcpp_reset.restype = I
     L.pcpp_query.argtypes = [P, C.POINTER(pcpp_info)]; L.pcpp_query.restype = I
     L.pcpp_destroy.argtypes = [P]; L.pcpp_destroy.restype = None
+    L.pcpp_profile.argtypes = [P, V, I, I, I, C.POINTER(pcpp_prof)]; L.pcpp_profile.restype = I
     L.pcpp_last_error.argtypes = []; L.pcpp_last_error.restype = C.c_char_p
     L.pcpp_op_conv.argtypes = [V, I, I, I, I, I, I, V, V, V, V, V, I, I, I, V]; L.pcpp_op_conv.restype = I
     L.pcpp_op_attention.argtypes = [V, C.POINTER(C.c_void_p), C.POINTER(C.c_int), I, I, I, I, I, V, I, I, V]
@@ -208,6 +213,13 @@ class Plan:
         info = pcpp_info()
         _chk(lib().pcpp_query(self.h, C.byref(info)), "pcpp_query")
         return info.as_dict()
+
+    def pcpp_profile(self, latent, kind_mask: int, sync: int = 0, iters: int = 5) -> dict:
+        """Device ms per step of the ops in kind_mask (1 GEMM/conv, 2 attention, 4 GN, 8 exchange,
+        16 other), measured in isolation, plus their algorithmic flops/bytes."""
+        pr = pcpp_prof()
+        _chk(lib().pcpp_profile(self.h, _ptr(latent), kind_mask, sync, iters, C.byref(pr)), "pcpp_profile")
+        return dict(ms=pr.ms, flops=pr.flops, bytes=pr.bytes, launches=pr.launches)
 
     def close(self):
         if self.h:

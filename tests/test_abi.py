@@ -29,6 +29,16 @@ def test_manifest_matches_oracle(model):
     assert pcpp.pcpp_weights_len(model) == sum(M.init_spec(s, k)[0] for _, s, k in M.manifest(model))
 
 
+@pytest.mark.parametrize("model", ["tiny", "sdxl"])
+def test_init_rule_from_library_manifest_matches_oracle(model):
+    from paper_2412_02962_b200 import inputs
+    a = inputs.init_specs(pcpp.manifest(model))
+    b = M.weight_specs(model)
+    assert len(a) == len(b)
+    for x, y in zip(a, b):
+        assert x[0] == y[0] and x[1] == y[1] and abs(x[2] - y[2]) < 1e-15 * max(1, y[2])
+
+
 @pytest.mark.parametrize("model,H,n,p", [("sdxl", 128, 8, 0.8), ("sdxl", 128, 4, 0.8), ("sdxl", 128, 2, 0.3),
                                          ("sdxl", 256, 8, 0.8), ("sdxl", 480, 8, 0.8), ("sdxl", 128, 8, 0.0),
                                          ("sdxl", 128, 8, 0.125), ("sdxl", 128, 8, 0.25), ("sdxl", 128, 8, 0.5),
