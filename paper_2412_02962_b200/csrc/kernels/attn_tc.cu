@@ -1,0 +1,303 @@
+// tcgen05 flash attention for partially conditioned attention (§3.3; Fig. 3), sm_100a.
+//
+// One CTA = 128 query tokens of one (batch b, head).  Q comes from the local fresh patch; the
+// key/value stream is the concatenation of up to three row sources [stale top band ; local fresh ;
+// stale bottom band] (Eq. 1; reading D13), each a [rows][B][W][2C] tensor read in place -- the
+// neighbour bands straight out of the receive buffers, no concat copy.
+//
+//   warp 0      TMA: Q once; K,V tiles of 128 keys (4-D boxes: 64 head dims x Wbox x 1 x Rbox)
+//   warp 1      MMA (one thread): S_j = Q K_j^T -> TMEM (double-buffered, 128 cols each);
+//               O_j = P_j V_j -> TMEM (64 cols), P_j from smem (K-major SW128), V_j MN-major
+//   warps 2-5   softmax: thread = query row; online max/sum in fp32; P_j -> bf16 smem;
+//               O accumulated in registers with the running rescale; normalise and store.
+#include <cuda.h>
+#include "../common.cuh"
+#include "../kernels.h"
+#include "../sm100.cuh"
+
+namespace pcpp {
+
+struct TcAttnParams {
+  CUtensorMap mq, mkv[3];
+  int nsrc, rows[3];
+  int h, W, B, C;
+  int Wbox, Rbox, nWt, ntiles;
+  unsigned box_bytes;
+  void* out;
+};
+
+namespace {
+constexpr int TILE = 128 * 128;              // bytes of one 128-token x 64-dim bf16 tile
+constexpr int SM_Q = 0;
+constexpr int SM_K = TILE;                   // 2 stages
+constexpr int SM_V = 3 * TILE;               // 2 stages
+constexpr int SM_P = 5 * TILE;               // 2 x 16 KB atoms (keys 0-63, 64-127)
+constexpr int SM_BAR = 7 * TILE;
+constexpr int ATTN_SMEM = 1024 + SM_BAR + 256;
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void tile_coords(const TcAttnParams& p, int j, int& s, int& r0, int& w0) {
+  // enumerate sources in order, then row tiles, then column tiles
+  s = 0;
+  int acc = 0;
+  for (; s < p.nsrc; ++s) {
+    const int nt = ((p.rows[s] + p.Rbox - 1) / p.Rbox) * p.nWt;
+    if (j < acc + nt) break;
+    acc += nt;
+  }
+  const int jj = j - acc;
+  r0 = (jj / p.nWt) * p.Rbox;
+  w0 = (jj % p.nWt) * p.Wbox;
+}
+
+__global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__ TcAttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;      // [2]
+  uint64_t* kv_empty = bars + 3;     // [2]
+  uint64_t* s_full = bars + 5;       // [2]
+  uint64_t* p_full = bars + 7;
+  uint64_t* o_full = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+  const int q_r0 = (qt / p.nWt) * p.Rbox, q_w0 = (qt % p.nWt) * p.Wbox;
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&p.mq);
+    for (int s = 0; s < p.nsrc; ++s) sm100::tma_prefetch(&p.mkv[s]);
+    sm100::mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) { sm100::mbar_init(&kv_full[i], 1); sm100::mbar_init(&kv_empty[i], 1); sm100::mbar_init(&s_full[i], 1); }
+    sm100::mbar_init(p_full, 128);
+    sm100::mbar_init(o_full, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(tmem_slot);
+  if (p.box_bytes < (unsigned)TILE) {
+    // partial key tiles: the rows past the TMA box must be finite (zero) for P V
+    uint4* z = reinterpret_cast<uint4*>(smem + SM_K);
+    for (int i = threadIdx.x; i < 4 * TILE / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    sm100::fence_proxy_async_smem();
+  }
+  sm100::fence_before();
+  __syncthreads();
+  sm100::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nt = p.ntiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      sm100::mbar_arrive_expect_tx(q_full, p.box_bytes);
+      sm100::tma_load_4d(smem + SM_Q, &p.mq, q_full, head * 64, q_w0, b, q_r0);
+      for (int j = 0; j < nt; ++j) {
+        const int st = j & 1;
+        sm100::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        int s, r0, w0;
+        tile_coords(p, j, s, r0, w0);
+        sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * p.box_bytes);
+        sm100::tma_load_4d(smem + SM_K + st * TILE, &p.mkv[s], &kv_full[st], head * 64, w0, b, r0);
+        sm100::tma_load_4d(smem + SM_V + st * TILE, &p.mkv[s], &kv_full[st], p.C + head * 64, w0, b, r0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
+      const uint32_t q_base = sm100::smem_u32(smem + SM_Q);
+      const uint32_t p_base = sm100::smem_u32(smem + SM_P);
+      sm100::mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        sm100::mbar_wait(&kv_full[st], (j >> 1) & 1);
+        sm100::fence_after();
+        const uint32_t k_base = sm100::smem_u32(smem + SM_K + st * TILE);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          sm100::mma_bf16_ss(tmem + st * 128, sm100::sdesc_sw128(q_base + k * 32, 16, 1024),
+                             sm100::sdesc_sw128(k_base + k * 32, 16, 1024), id_s, k != 0);
+        sm100::mma_commit(&s_full[st]);
+      };
+      if (nt > 0) issue_s(0);
+      for (int j = 0; j < nt; ++j) {
+        const int st = j & 1;
+        if (j + 1 < nt) issue_s(j + 1);
+        sm100::mbar_wait(p_full, j & 1);
+        sm100::fence_after();
+        const uint32_t v_base = sm100::smem_u32(smem + SM_V + st * TILE);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          sm100::mma_bf16_ss(tmem + 256, sm100::sdesc_sw128(p_base + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
+                             sm100::sdesc_sw128(v_base + k * 2048, 16384, 1024), id_o, k != 0);
+        sm100::mma_commit(o_full);
+        sm100::mma_commit(&kv_empty[st]);
+      }
+    }
+  } else {
+    // softmax warpgroup: TMEM lane quarter = warp % 4, thread = query row
+    const int qw = warp & 3;
+    const int row = qw * 32 + lane;
+    const uint32_t trow = tmem + (uint32_t(qw * 32) << 16);
+    const float sl2 = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
+    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+    float acc[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+    uint8_t* P = smem + SM_P;
+    for (int j = 0; j < nt; ++j) {
+      const int st = j & 1;
+      int s, r0, w0;
+      tile_coords(p, j, s, r0, w0);
+      const int nvr = min(p.Rbox, p.rows[s] - r0);         // valid rows in this key tile
+      const int nvw = min(p.Wbox, p.W - w0);               // valid cols
+      // keys are a contiguous valid prefix: Rbox > 1 only when Wbox == W (full rows)
+      const int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;
+      sm100::mbar_wait(&s_full[st], (j >> 1) & 1);
+      sm100::fence_after();
+      // pass 1: row max over valid keys
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t v[32];
+        sm100::tmem_ld32(trow + st * 128 + c, v);
+        sm100::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = c + i;
+          mx = key < nvalid ? fmaxf(mx, __uint_as_float(v[i])) : mx;
+        }
+      }
+      const float m_new = fmaxf(m, mx * sl2);
+      const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_new);
+      // fold O_{j-1} into the register accumulator (it was computed with max m_{j-1})
+      if (j > 0) {
+        sm100::mbar_wait(o_full, (j - 1) & 1);
+        sm100::fence_after();
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          uint32_t v[32];
+          sm100::tmem_ld32(trow + 256 + c, v);
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[c + i] = acc[c + i] * alpha_prev + __uint_as_float(v[i]);
+        }
+      }
+      // pass 2: p = exp2(s*scale - m_new) -> bf16 P (K-major SW128), row sum
+      float ls = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t v[32];
+        sm100::tmem_ld32(trow + st * 128 + c, v);
+        sm100::tmem_wait_ld();
+        float pv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = c + i;
+          pv[i] = key < nvalid ? fast_exp2(__uint_as_float(v[i]) * sl2 - m_new) : 0.f;
+          ls += pv[i];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int key0 = c + 8 * u;
+          const int atom = key0 >> 6, chunk = (key0 & 63) >> 3;
+          uint8_t* dst = P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4);
+          store8(reinterpret_cast<bf16*>(dst), pv + 8 * u);
+        }
+      }
+      l = l * alpha + ls;
+      m = m_new;
+      alpha_prev = alpha;
+      sm100::fence_proxy_async_smem();
+      sm100::fence_before();
+      sm100::mbar_arrive(p_full);
+    }
+    if (nt > 0) {
+      sm100::mbar_wait(o_full, (nt - 1) & 1);
+      sm100::fence_after();
+#pragma unroll
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t v[32];
+        sm100::tmem_ld32(trow + 256 + c, v);
+        sm100::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[c + i] = acc[c + i] * alpha_prev + __uint_as_float(v[i]);
+      }
+    }
+    const int ri = row / p.Wbox, wi = row % p.Wbox;
+    const int r = q_r0 + ri, w = q_w0 + wi;
+    if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
+      const float inv = 1.f / l;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc[i] *= inv;
+      bf16* o = reinterpret_cast<bf16*>(p.out) + (((long long)r * p.B + b) * p.W + w) * p.C + head * 64;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) store8(o + 8 * u, acc + 8 * u);
+    }
+  }
+  sm100::fence_before();
+  __syncthreads();
+  if (warp == 1) sm100::tmem_dealloc<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+void* tma_encode_fn();
+
+static bool encode_tok(CUtensorMap* m, const void* base, int rows, int B, int W, int Cst, int Wbox, int Rbox) {
+  auto f = reinterpret_cast<EncodeTiledFn>(tma_encode_fn());
+  cuuint64_t dims[4] = {(cuuint64_t)Cst, (cuuint64_t)W, (cuuint64_t)B, (cuuint64_t)rows};
+  cuuint64_t strides[3] = {(cuuint64_t)Cst * 2, (cuuint64_t)W * Cst * 2, (cuuint64_t)B * W * Cst * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)Wbox, 1, (cuuint32_t)Rbox};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool attn_tc_supported(const AttnArgs& a) {
+  if (a.dtype != DT_BF16 || a.C % 64 || a.nsrc < 1) return false;
+  if (!tma_encode_fn()) return false;
+  return true;
+}
+
+void attn_tc_init() {
+  cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATTN_SMEM);
+}
+
+bool launch_attn_tc(const AttnArgs& a, cudaStream_t s) {
+  TcAttnParams p;
+  memset(&p, 0, sizeof p);
+  p.h = a.h; p.W = a.W; p.B = a.B; p.C = a.C; p.out = a.out;
+  if (a.W >= 128) { p.Wbox = 128; p.Rbox = 1; }
+  else if (128 % a.W == 0) { p.Wbox = a.W; p.Rbox = 128 / a.W; }
+  else { p.Wbox = a.W; p.Rbox = 1; }
+  p.nWt = (a.W + p.Wbox - 1) / p.Wbox;
+  p.box_bytes = 128u * p.Wbox * p.Rbox;
+  if (!encode_tok(&p.mq, a.q, a.h, a.B, a.W, a.C, p.Wbox, p.Rbox)) return false;
+  p.nsrc = 0;
+  p.ntiles = 0;
+  for (int i = 0; i < a.nsrc; ++i) {
+    if (a.src[i].rows <= 0) continue;
+    if (!encode_tok(&p.mkv[p.nsrc], a.src[i].kv, a.src[i].rows, a.B, a.W, 2 * a.C, p.Wbox, p.Rbox)) return false;
+    p.rows[p.nsrc] = a.src[i].rows;
+    p.ntiles += ((a.src[i].rows + p.Rbox - 1) / p.Rbox) * p.nWt;
+    p.nsrc++;
+  }
+  for (int i = p.nsrc; i < 3; ++i) p.mkv[i] = p.mkv[0];
+  const int qtiles = ((a.h + p.Rbox - 1) / p.Rbox) * p.nWt;
+  dim3 grid(qtiles, a.C / 64, a.B);
+  attn_tc_kernel<<<grid, 192, ATTN_SMEM, s>>>(p);
+  return true;
+}
+
+}  // namespace pcpp

@@ -15,8 +15,12 @@ void launch_gemm_auto(const GemmArgs& g, bool allow_tc, cudaStream_t s) {
   if (allow_tc && gemm_tc_supported(g) && launch_gemm_tc(g, s)) return;
   launch_gemm_simt(g, s);
 }
+bool attn_tc_supported(const AttnArgs& a);
+bool launch_attn_tc(const AttnArgs& a, cudaStream_t s);
+void attn_tc_init();
+
 void launch_attn_auto(const AttnArgs& a, bool allow_tc, cudaStream_t s) {
-  (void)allow_tc;
+  if (allow_tc && attn_tc_supported(a) && launch_attn_tc(a, s)) return;
   launch_attn_simt(a, s);
 }
 void launch_gemm_tc_or_simt(const Plan& P, const GemmArgs& g, cudaStream_t s) { launch_gemm_auto(g, P.use_tc, s); }
@@ -28,6 +32,7 @@ void kernels_init() {
   done = true;
   gn_init();
   gemm_tc_init();
+  attn_tc_init();
 }
 
 }  // namespace pcpp

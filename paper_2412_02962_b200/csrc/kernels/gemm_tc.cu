@@ -184,6 +184,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 bool tc_available() { return encode_fn() != nullptr; }
+void* tma_encode_fn() { return reinterpret_cast<void*>(encode_fn()); }
 
 // 4-D map over a [rows(+2 pad)][B][W][C] bf16 activation tensor; box (64, Wbox, Bbox, Rbox)
 static bool encode_act(CUtensorMap* m, const ActView& v, int pad, int Wbox, int Bbox, int Rbox) {
