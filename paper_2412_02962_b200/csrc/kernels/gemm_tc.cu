@@ -20,7 +20,7 @@ namespace pcpp {
 
 struct TcGemmParams {
   CUtensorMap ma0, ma1, mb;
-  int nk0, nkc, taps, pad;
+  int nk0, nkc, taps, pad, stride;
   int rows_out, w_out, B;
   int Wbox, Bbox, Rbox, nWt, m_tiles;
   int N, n_split;
@@ -82,9 +82,9 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
         const int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
         sm100::mbar_arrive_expect_tx(&full[st], p.a_bytes + Cfg::B_BYTES);
         if (kc < p.nk0)
-          sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma0, &full[st], kc * 64, w0 + dw, b0, r0 + dr + p.pad);
+          sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma0, &full[st], kc * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
         else
-          sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma1, &full[st], (kc - p.nk0) * 64, w0 + dw, b0, r0 + dr + p.pad);
+          sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma1, &full[st], (kc - p.nk0) * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
         sm100::tma_load_2d(sB + st * Cfg::B_BYTES, &p.mb, &full[st], s * 64, n0);
       }
     }
@@ -186,14 +186,16 @@ static EncodeTiledFn encode_fn() {
 bool tc_available() { return encode_fn() != nullptr; }
 void* tma_encode_fn() { return reinterpret_cast<void*>(encode_fn()); }
 
-// 4-D map over a [rows(+2 pad)][B][W][C] bf16 activation tensor; box (64, Wbox, Bbox, Rbox)
-static bool encode_act(CUtensorMap* m, const ActView& v, int pad, int Wbox, int Bbox, int Rbox) {
+// 4-D map over a [rows(+2 pad)][B][W][C] bf16 activation tensor; box (64, Wbox, Bbox, Rbox) output
+// tokens.  Stride-2 convs use TMA element strides 2 along W and rows: the box spans 2*Wbox x 2*Rbox
+// input elements and delivers every second one (Wbox x Rbox), so A stays one dense SW128 tile.
+static bool encode_act(CUtensorMap* m, const ActView& v, int pad, int Wbox, int Bbox, int Rbox, int stride) {
   const size_t es = 2;
   char* base = reinterpret_cast<char*>(v.base) - (size_t)pad * v.B * v.W * v.C * es;
   cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.B, (cuuint64_t)(v.rows + 2 * pad)};
   cuuint64_t strides[3] = {(cuuint64_t)v.C * es, (cuuint64_t)v.W * v.C * es, (cuuint64_t)v.B * v.W * v.C * es};
-  cuuint32_t box[4] = {64, (cuuint32_t)Wbox, (cuuint32_t)Bbox, (cuuint32_t)Rbox};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)(Wbox * stride), (cuuint32_t)Bbox, (cuuint32_t)(Rbox * stride)};
+  cuuint32_t estr[4] = {1, (cuuint32_t)stride, 1, (cuuint32_t)stride};
   return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -222,7 +224,7 @@ bool gemm_tc_supported(const GemmArgs& g) {
   if (!tc_available()) return false;
   if (g.a0.dtype != DT_BF16 || g.wdtype != DT_BF16) return false;
   if (g.a1.base && g.a1.dtype != DT_BF16) return false;
-  if (g.stride != 1) return false;
+  if (g.stride != 1 && !(g.stride == 2 && g.taps == 9)) return false;
   if (g.cin % 64 || g.c0 % 64) return false;
   if (g.out.dtype != DT_BF16 && g.out.dtype != DT_F32) return false;
   if (g.res.base && g.res.dtype != DT_BF16) return false;
@@ -256,15 +258,15 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   p.nWt = (g.w_out + p.Wbox - 1) / p.Wbox;
   if (p.Bbox == 2) p.m_tiles = (g.rows_out + p.Rbox - 1) / p.Rbox;
   else p.m_tiles = g.rows_out * g.B * p.nWt;
-  p.taps = g.taps; p.pad = g.taps == 9 ? 1 : 0;
+  p.taps = g.taps; p.pad = g.taps == 9 ? 1 : 0; p.stride = g.stride;
   p.nkc = g.cin / 64; p.nk0 = g.c0 / 64;
   p.rows_out = g.rows_out; p.w_out = g.w_out; p.B = g.B;
   p.N = g.N; p.n_split = g.n_split < g.N ? g.n_split : (1 << 30);
   p.a_bytes = 128u * p.Wbox * p.Bbox * p.Rbox;
   p.bias = g.bias; p.temb = g.temb; p.temb_ld = g.temb_ld;
   p.res = g.res; p.out = g.out; p.out2 = g.out2;
-  if (!encode_act(&p.ma0, g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox)) return false;
-  if (!encode_act(&p.ma1, g.a1.base ? g.a1 : g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox)) return false;
+  if (!encode_act(&p.ma0, g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
+  if (!encode_act(&p.ma1, g.a1.base ? g.a1 : g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN)) return false;
   switch (BN) {
     case 256: launch_bn<256>(p, s); break;
