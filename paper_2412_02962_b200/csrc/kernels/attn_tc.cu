@@ -7,9 +7,9 @@
 //
 //   warp 0      TMA: Q once; K,V tiles of 128 keys (4-D boxes: 64 head dims x Wbox x 1 x Rbox)
 //   warp 1      MMA (one thread): S_j = Q K_j^T -> TMEM (double-buffered, 128 cols each);
-//               O_j = P_j V_j -> TMEM (64 cols), P_j from smem (K-major SW128), V_j MN-major
-//   warps 2-5   softmax: thread = query row; online max/sum in fp32; P_j -> bf16 smem;
-//               O accumulated in registers with the running rescale; normalise and store.
+//               O += P_j V_j -> TMEM (64 cols), P_j from smem (K-major SW128), V_j MN-major
+//   warps 2-5   softmax: thread = query row; S row held in registers (one TMEM read), online
+//               max/sum in fp32 with lazy rescale of the TMEM accumulator; P_j -> bf16 smem.
 #include <cuda.h>
 #include "../common.cuh"
 #include "../kernels.h"
@@ -136,21 +136,20 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           sm100::mma_bf16_ss(tmem + 256, sm100::sdesc_sw128(p_base + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
-                             sm100::sdesc_sw128(v_base + k * 2048, 16384, 1024), id_o, k != 0);
+                             sm100::sdesc_sw128(v_base + k * 2048, 16384, 1024), id_o, (j | k) != 0);
         sm100::mma_commit(o_full);
         sm100::mma_commit(&kv_empty[st]);
       }
     }
   } else {
-    // softmax warpgroup: TMEM lane quarter = warp % 4, thread = query row
+    // softmax warpgroup: TMEM lane quarter = warp % 4, thread = query row.  O accumulates in
+    // TMEM across key tiles; the running max is only raised (and O, l rescaled) when a tile's max
+    // exceeds it by more than 2^8, so most tiles need no rescale (p <= 256 stays exact in fp32).
     const int qw = warp & 3;
     const int row = qw * 32 + lane;
     const uint32_t trow = tmem + (uint32_t(qw * 32) << 16);
     const float sl2 = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
-    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-    float acc[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+    float m = -INFINITY, l = 0.f;
     uint8_t* P = smem + SM_P;
     for (int j = 0; j < nt; ++j) {
       const int st = j & 1;
@@ -162,59 +161,51 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
       const int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;
       sm100::mbar_wait(&s_full[st], (j >> 1) & 1);
       sm100::fence_after();
-      // pass 1: row max over valid keys
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t v[32];
-        sm100::tmem_ld32(trow + st * 128 + c, v);
-        sm100::tmem_wait_ld();
+      float sv[128];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int key = c + i;
-          mx = key < nvalid ? fmaxf(mx, __uint_as_float(v[i])) : mx;
-        }
+      for (int c = 0; c < 128; c += 32) sm100::tmem_ld32(trow + st * 128 + c, reinterpret_cast<uint32_t*>(sv + c));
+      sm100::tmem_wait_ld();
+      float mx = -INFINITY;
+      if (nvalid >= 128) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) mx = fmaxf(mx, sv[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) { if (i >= nvalid) sv[i] = -INFINITY; mx = fmaxf(mx, sv[i]); }
       }
-      const float m_new = fmaxf(m, mx * sl2);
-      const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_new);
-      // fold O_{j-1} into the register accumulator (it was computed with max m_{j-1})
+      mx *= sl2;
+      const bool raise = mx > m + 8.0f;
+      const float m_new = raise ? mx : m;
+      const float alpha = raise ? (m == -INFINITY ? 0.f : fast_exp2(m - m_new)) : 1.f;
+      // O_{j-1} must be complete before P_j overwrites P_{j-1} and before O is rescaled
       if (j > 0) {
         sm100::mbar_wait(o_full, (j - 1) & 1);
         sm100::fence_after();
+        if (__any_sync(0xffffffffu, raise)) {
 #pragma unroll
-        for (int c = 0; c < 64; c += 32) {
-          uint32_t v[32];
-          sm100::tmem_ld32(trow + 256 + c, v);
-          sm100::tmem_wait_ld();
+          for (int c = 0; c < 64; c += 16) {
+            uint32_t v[16];
+            sm100::tmem_ld16(trow + 256 + c, v);
+            sm100::tmem_wait_ld();
+            uint32_t o16[16];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[c + i] = acc[c + i] * alpha_prev + __uint_as_float(v[i]);
+            for (int i = 0; i < 16; ++i) o16[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            sm100::tmem_st16(trow + 256 + c, o16);
+          }
+          sm100::tmem_wait_st();
         }
       }
-      // pass 2: p = exp2(s*scale - m_new) -> bf16 P (K-major SW128), row sum
       float ls = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t v[32];
-        sm100::tmem_ld32(trow + st * 128 + c, v);
-        sm100::tmem_wait_ld();
-        float pv[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int key = c + i;
-          pv[i] = key < nvalid ? fast_exp2(__uint_as_float(v[i]) * sl2 - m_new) : 0.f;
-          ls += pv[i];
-        }
+      for (int c = 0; c < 128; c += 8) {
+        float pv[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int key0 = c + 8 * u;
-          const int atom = key0 >> 6, chunk = (key0 & 63) >> 3;
-          uint8_t* dst = P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4);
-          store8(reinterpret_cast<bf16*>(dst), pv + 8 * u);
-        }
+        for (int i = 0; i < 8; ++i) { pv[i] = fast_exp2(fmaf(sv[c + i], sl2, -m_new)); ls += pv[i]; }
+        const int atom = c >> 6, chunk = (c & 63) >> 3;
+        store8(reinterpret_cast<bf16*>(P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4)), pv);
       }
       l = l * alpha + ls;
       m = m_new;
-      alpha_prev = alpha;
       sm100::fence_proxy_async_smem();
       sm100::fence_before();
       sm100::mbar_arrive(p_full);
@@ -222,15 +213,11 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
     if (nt > 0) {
       sm100::mbar_wait(o_full, (nt - 1) & 1);
       sm100::fence_after();
-#pragma unroll
-      for (int c = 0; c < 64; c += 32) {
-        uint32_t v[32];
-        sm100::tmem_ld32(trow + 256 + c, v);
-        sm100::tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[c + i] = acc[c + i] * alpha_prev + __uint_as_float(v[i]);
-      }
     }
+    float acc[64];
+#pragma unroll
+    for (int c = 0; c < 64; c += 32) sm100::tmem_ld32(trow + 256 + c, reinterpret_cast<uint32_t*>(acc + c));
+    sm100::tmem_wait_ld();
     const int ri = row / p.Wbox, wi = row % p.Wbox;
     const int r = q_r0 + ri, w = q_w0 + wi;
     if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {

@@ -27,11 +27,11 @@ __host__ __device__ __forceinline__ Lanes lanes_for(int C) {
 }
 }  // namespace
 
-int gn_stats_chunks(int rows, int W) {
-  long long tok = (long long)rows * W;
+int gn_stats_chunks(int rows, int W) {   // CTAs of gn_stats (each covers both CFG branches)
+  long long tok = (long long)rows * 2 * W;
   long long c = tok / 32;                 // >= 32 tokens per chunk
   if (c < 1) c = 1;
-  if (c > 128) c = 128;                   // x B = 2 -> up to 256 CTAs
+  if (c > 296) c = 296;                   // 2 CTAs per SM
   return (int)c;
 }
 
@@ -41,73 +41,88 @@ __device__ __forceinline__ const T* vptr(const ActView& v, long long rowtok, int
 }
 
 // ---- stats -------------------------------------------------------------------------------------
+// CTA `chunk` covers layout tokens [T0, T1) (all (r, b, w) in memory order: address T*C + c, no
+// index division); token lanes stride by ntl, 4 independent 16 B loads in flight per thread.
 template <typename T>
 __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
-  extern __shared__ float red[];                   // [ntl][nv][16]
-  __shared__ double chs[2][2560];
+  extern __shared__ float red[];                   // [ntl][nv][2 b][8][2]
   __shared__ bool amlast;
-  const int b = blockIdx.y, chunk = blockIdx.x;
+  const int chunk = blockIdx.x;
   const int W = a.x0.W, B = a.x0.B, C = a.C;
   const Lanes L = lanes_for(C);
   const int tid = threadIdx.x;
   const int vl = tid % L.nvl, tl = tid / L.nvl;
-  const long long ntok = (long long)a.x0.rows * W;
-  const long long t0 = ntok * chunk / a.nchunk, t1 = ntok * (chunk + 1) / a.nchunk;
-  float s[2][8], q[2][8];
+  const long long ntok = (long long)a.x0.rows * B * W;
+  const long long T0 = ntok * chunk / a.nchunk, T1 = ntok * (chunk + 1) / a.nchunk;
+  float s[2][2][8], q[2][2][8];                    // [u][b][e]
 #pragma unroll
   for (int u = 0; u < 2; ++u)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) { s[u][e] = 0.f; q[u][e] = 0.f; }
+    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { s[u][bb][e] = 0.f; q[u][bb][e] = 0.f; }
   if (tl < L.ntl) {
-    long long t = t0 + tl;
-    int r = (int)(t / W), w = (int)(t % W);
-    for (; t < t1; t += L.ntl) {
-      const long long rowtok = ((long long)r * B + b) * W + w;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (u >= L.vpt) break;
-        const int v = vl * L.vpt + u;
-        if (v >= L.nv) break;
-        const int c = v * 8;
-        float x[8];
-        if (c < a.c0) load8(vptr<T>(a.x0, rowtok, c), x); else load8(vptr<T>(a.x1, rowtok, c - a.c0), x);
+    for (int u = 0; u < 2; ++u) {
+      const int v = vl * L.vpt + u;
+      if (u >= L.vpt || v >= L.nv) continue;
+      const int c = v * 8;
+      const bool second = c >= a.c0;
+      const ActView& src = second ? a.x1 : a.x0;
+      const int cc = second ? c - a.c0 : c;
+      long long Tt = T0 + tl;
+      int w = (int)(Tt % W), bq = (int)((Tt / W) % B);
+      for (; Tt < T1; Tt += 4LL * L.ntl) {
+        float x[4][8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) { s[u][e] += x[e]; q[u][e] = fmaf(x[e], x[e], q[u][e]); }
+        for (int k = 0; k < 4; ++k) {
+          const long long Tk = Tt + (long long)k * L.ntl;
+          if (Tk < T1) load8(vptr<T>(src, Tk, cc), x[k]);
+          else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[k][e] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float xv = x[k][e];
+            if (bq == 0) { s[u][0][e] += xv; q[u][0][e] = fmaf(xv, xv, q[u][0][e]); }
+            else         { s[u][1][e] += xv; q[u][1][e] = fmaf(xv, xv, q[u][1][e]); }
+          }
+          w += L.ntl;
+          while (w >= W) { w -= W; bq = (bq + 1 == B) ? 0 : bq + 1; }
+        }
       }
-      w += L.ntl;
-      while (w >= W) { w -= W; ++r; }
     }
   }
-  for (int u = 0; u < L.vpt; ++u) {
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
     const int v = vl * L.vpt + u;
-    if (tl < L.ntl && v < L.nv)
+    if (u < L.vpt && tl < L.ntl && v < L.nv)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        red[((long long)tl * L.nv + v) * 16 + e * 2 + 0] = s[u][e];
-        red[((long long)tl * L.nv + v) * 16 + e * 2 + 1] = q[u][e];
-      }
-  }
-  __syncthreads();
-  for (int c = tid; c < C; c += NT) {                // fixed-order reduction over token lanes
-    const int v = c / 8, e = c % 8;
-    double ss = 0.0, qq = 0.0;
-    for (int l = 0; l < L.ntl; ++l) {
-      ss += red[((long long)l * L.nv + v) * 16 + e * 2 + 0];
-      qq += red[((long long)l * L.nv + v) * 16 + e * 2 + 1];
-    }
-    chs[0][c] = ss; chs[1][c] = qq;
+      for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          red[(((long long)tl * L.nv + v) * 2 + bb) * 16 + e * 2 + 0] = s[u][bb][e];
+          red[(((long long)tl * L.nv + v) * 2 + bb) * 16 + e * 2 + 1] = q[u][bb][e];
+        }
   }
   __syncthreads();
   const int cg = C / G;
-  if (tid < 2 * G) {                                  // partial layout [B][G][2][nchunk]
-    const int g = tid >> 1, k = tid & 1;
+  if (tid < B * G * 2) {                             // fixed-order per-(b, g, stat) sums -> partial [B][G][2][nchunk]
+    const int bb = tid / (2 * G), g = (tid >> 1) % G, k = tid & 1;
     double acc = 0.0;
-    for (int c = g * cg; c < (g + 1) * cg; ++c) acc += chs[k][c];
-    a.partial[(((long long)b * G + g) * 2 + k) * a.nchunk + chunk] = acc;
+    for (int c = g * cg; c < (g + 1) * cg; ++c) {
+      const int v = c / 8, e = c % 8;
+      for (int l = 0; l < L.ntl; ++l) acc += red[(((long long)l * L.nv + v) * 2 + bb) * 16 + e * 2 + k];
+    }
+    a.partial[(((long long)bb * G + g) * 2 + k) * a.nchunk + chunk] = acc;
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) amlast = (atomicAdd(a.counter, 1u) == gridDim.x * gridDim.y - 1);
+  if (tid == 0) amlast = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
   __syncthreads();
   if (!amlast) return;
   __threadfence();
@@ -126,10 +141,9 @@ __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
 
 void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
   const Lanes L = lanes_for(a.C);
-  const size_t smem = (size_t)L.ntl * L.nv * 16 * sizeof(float);
-  dim3 grid(a.nchunk, a.x0.B);
-  if (a.x0.dtype == DT_F32) gn_stats_kernel<float><<<grid, NT, smem, s>>>(a);
-  else gn_stats_kernel<bf16><<<grid, NT, smem, s>>>(a);
+  const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
+  if (a.x0.dtype == DT_F32) gn_stats_kernel<float><<<a.nchunk, NT, smem, s>>>(a);
+  else gn_stats_kernel<bf16><<<a.nchunk, NT, smem, s>>>(a);
 }
 
 // ---- apply -------------------------------------------------------------------------------------
@@ -183,27 +197,36 @@ __global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int t
   const long long ntok = (long long)a.x0.rows * B * W;           // (r, b, w) tokens in layout order
   const long long T0 = (long long)blockIdx.x * tok_per_cta;
   const long long T1 = T0 + tok_per_cta < ntok ? T0 + tok_per_cta : ntok;
-  long long T = T0 + tl;
-  int w = (int)(T % W);
-  long long rb = T / W;
-  for (; T < T1; T += L.ntl) {
-    const int b = (int)(rb % B);
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      if (cvec[u] < 0) continue;
-      const int c = cvec[u];
-      float x[8];
-      if (c < a.c0) load8(vptr<TI>(a.x0, T, c), x); else load8(vptr<TI>(a.x1, T, c - a.c0), x);
+  for (int u = 0; u < 2; ++u) {
+    if (cvec[u] < 0) continue;
+    const int c = cvec[u];
+    const bool second = c >= a.c0;
+    const ActView& src = second ? a.x1 : a.x0;
+    const int cc = second ? c - a.c0 : c;
+    long long T = T0 + tl;
+    int w = (int)(T % W), bq = (int)((T / W) % B);
+    for (; T < T1; T += 4LL * L.ntl) {
+      float x[4][8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float y = fmaf(x[e], b ? A[u][1][e] : A[u][0][e], b ? Bc[u][1][e] : Bc[u][0][e]);
-        x[e] = a.silu ? silu_f(y) : y;
+      for (int k = 0; k < 4; ++k) {
+        const long long Tk = T + (long long)k * L.ntl;
+        if (Tk < T1) load8(vptr<TI>(src, Tk, cc), x[k]);
       }
-      // out has the same (r, b, w) geometry; it may be a padded tensor (base = row 0)
-      store8(reinterpret_cast<TO*>(a.out.base) + T * a.out.C + c, x);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long long Tk = T + (long long)k * L.ntl;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float y = fmaf(x[k][e], bq ? A[u][1][e] : A[u][0][e], bq ? Bc[u][1][e] : Bc[u][0][e]);
+          x[k][e] = a.silu ? silu_f(y) : y;
+        }
+        // out has the same (r, b, w) geometry; it may be a padded tensor (base = row 0)
+        if (Tk < T1) store8(reinterpret_cast<TO*>(a.out.base) + Tk * a.out.C + c, x[k]);
+        w += L.ntl;
+        while (w >= W) { w -= W; bq = (bq + 1 == B) ? 0 : bq + 1; }
+      }
     }
-    w += L.ntl;
-    while (w >= W) { w -= W; ++rb; }
   }
 }
 
@@ -217,9 +240,9 @@ void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
   else gn_apply_kernel<bf16, bf16><<<(unsigned)blocks, NT, 0, s>>>(a, (int)per);
 }
 
-void gn_init() {   // dynamic smem <= 40 KB (C <= 2560) on top of 40 KB static
-  cudaFuncSetAttribute(gn_stats_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
-  cudaFuncSetAttribute(gn_stats_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+void gn_init() {   // dynamic smem: ntl * nv * 32 floats <= 40 KB (C <= 2560)
+  cudaFuncSetAttribute(gn_stats_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(gn_stats_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
 }
 
 }  // namespace pcpp
