@@ -129,6 +129,15 @@ PCPP_API pcpp_status pcpp_plan(int H, int W, int C, int n_patches, double cond_f
 PCPP_API pcpp_status pcpp_plan_info(int H, int W, int C, int n_patches, double cond_fraction, int warmup_steps,
                            const pcpp_config* cfg, pcpp_info* info);
 
+/* Host-only: the NCCL issue schedule of rank cfg->rank for one step (sync = warm-up step or not).
+ * Writes up to cap records of 5 ints {op (0 send, 1 recv, 2 all-gather), peer (-1 for all-gather),
+ * bytes, class (0 attn, 1 conv, 2 gn), group (exchange ordinal; ops of one group are issued inside
+ * one ncclGroupStart/End)} in issue order; returns the record count (or -1 on invalid arguments).
+ * Every rank issues its groups in the same layer order, so tagless NCCL p2p matching pairs the
+ * k-th send a->b with the k-th recv b<-a (App. A). */
+PCPP_API int pcpp_plan_schedule(int H, int W, int C, int n_patches, double cond_fraction, int warmup_steps,
+                                const pcpp_config* cfg, int sync, int* out, int cap);
+
 /* ---- execution ----------------------------------------------------------------------------- */
 
 /* Set the condition vector c (HOST, temb-dim floats: 1280 SDXL / 512 tiny); the cond branch adds

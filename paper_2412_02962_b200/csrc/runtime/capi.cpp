@@ -11,6 +11,7 @@
 
 namespace pcpp {
 const char* last_error_msg();
+XGroup make_group_public(const Plan& P, const Op& op, int sync, int par, std::vector<Xfer>& lb);
 void launch_gemm_auto(const GemmArgs& g, bool allow_tc, cudaStream_t s);
 void launch_attn_auto(const AttnArgs& a, bool allow_tc, cudaStream_t s);
 bool tc_available();
@@ -155,6 +156,32 @@ pcpp_status pcpp_plan_info(int H, int W, int C, int n, double p, int w, const pc
   fill_info(P, info);
   return PCPP_OK;
   GUARD_END
+}
+
+int pcpp_plan_schedule(int H, int W, int C, int n, double p, int w, const pcpp_config* cfg, int sync, int* out, int cap) {
+  try {
+    Plan P;
+    if (setup_plan(P, H, W, C, n, p, w, cfg) != PCPP_OK) return -1;
+    const int me = cfg->comm_backend == PCPP_COMM_NCCL ? cfg->rank : 0;
+    int cnt = 0, grp = 0;
+    auto put = [&](int op, int peer, long long bytes, int cls, int g) {
+      if (out && cnt < cap) { int* r = out + 5 * cnt; r[0] = op; r[1] = peer; r[2] = (int)bytes; r[3] = cls; r[4] = g; }
+      ++cnt;
+    };
+    std::vector<Xfer> lb;
+    for (const Op& op : P.ops) {
+      if (!((op.k == OP_HALO || op.k == OP_KVX || op.k == OP_GN) && P.n > 1)) continue;
+      XGroup G = make_group_public(P, op, sync ? 1 : 0, 0, lb);
+      if (G.allgather) put(2, -1, (long long)G.ag_bytes, G.cls, grp);
+      else
+        for (const Xfer& x : G.remote) {
+          if (x.src_rank == me) put(0, x.dst_rank, (long long)x.bytes, x.cls, grp);
+          if (x.dst_rank == me) put(1, x.src_rank, (long long)x.bytes, x.cls, grp);
+        }
+      ++grp;
+    }
+    return cnt;
+  } catch (...) { return -1; }
 }
 
 pcpp_status pcpp_plan(int H, int W, int C, int n, double p, int w, const pcpp_config* cfg, pcpp_plan_t* out) {

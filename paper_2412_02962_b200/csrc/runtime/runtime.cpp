@@ -264,6 +264,10 @@ static XGroup make_group(const Plan& P, const Op& op, int sync, int par, std::ve
   return G;
 }
 
+XGroup make_group_public(const Plan& P, const Op& op, int sync, int par, std::vector<Xfer>& lb) {
+  return make_group(P, op, sync, par, lb);
+}
+
 pcpp_status plan_build_exchanges(Plan& P) {
   P.op_xord.assign(P.ops.size(), -1);
   int nx = 0;

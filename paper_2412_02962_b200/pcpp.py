@@ -55,7 +55,7 @@ class pcpp_prof(C.Structure):
     _fields_ = [("ms", C.c_double), ("flops", C.c_double), ("bytes", C.c_double), ("launches", C.c_int)]
 
 
-SYMBOLS = ["pcpp_profile", "pcpp_config_default", "pcpp_get_unique_id", "pcpp_weights_len", "pcpp_manifest_count",
+SYMBOLS = ["pcpp_plan_schedule", "pcpp_profile", "pcpp_config_default", "pcpp_get_unique_id", "pcpp_weights_len", "pcpp_manifest_count",
            "pcpp_manifest_entry", "pcpp_plan", "pcpp_plan_info", "pcpp_set_cond", "pcpp_step",
            "pcpp_sample", "pcpp_reset", "pcpp_query", "pcpp_destroy", "pcpp_last_error",
            "pcpp_op_conv", "pcpp_op_attention", "pcpp_op_groupnorm", "pcpp_op_pack_rows",
@@ -86,6 +86,8 @@ def lib():
     L.pcpp_reset.argtypes = [P]; L.pcpp_reset.restype = I
     L.pcpp_query.argtypes = [P, C.POINTER(pcpp_info)]; L.pcpp_query.restype = I
     L.pcpp_destroy.argtypes = [P]; L.pcpp_destroy.restype = None
+    L.pcpp_plan_schedule.argtypes = [I, I, I, I, D, I, C.POINTER(pcpp_config), I, C.POINTER(C.c_int), I]
+    L.pcpp_plan_schedule.restype = I
     L.pcpp_profile.argtypes = [P, V, I, I, I, C.POINTER(pcpp_prof)]; L.pcpp_profile.restype = I
     L.pcpp_last_error.argtypes = []; L.pcpp_last_error.restype = C.c_char_p
     L.pcpp_op_conv.argtypes = [V, I, I, I, I, I, I, V, V, V, V, V, I, I, I, V]; L.pcpp_op_conv.restype = I
@@ -167,6 +169,17 @@ def make_config(model="sdxl", num_steps=50, guidance=5.0, precision="bf16", sche
         cfg.nccl_id = C.cast(cfg._id_buf, C.c_void_p)
     cfg.stream = stream
     return cfg
+
+
+def pcpp_plan_schedule(H, W, Cl, n, p, warmup, cfg, sync: int):
+    """This rank's NCCL issue schedule for one step: [(op, peer, bytes, cls, group)]."""
+    L = lib()
+    cnt = L.pcpp_plan_schedule(H, W, Cl, n, float(p), warmup, C.byref(cfg), int(sync), None, 0)
+    if cnt < 0:
+        raise PcppError(ERR_INVALID, "pcpp_plan_schedule")
+    buf = (C.c_int * (5 * max(cnt, 1)))()
+    L.pcpp_plan_schedule(H, W, Cl, n, float(p), warmup, C.byref(cfg), int(sync), buf, cnt)
+    return [tuple(buf[5 * i:5 * i + 5]) for i in range(cnt)]
 
 
 def pcpp_plan_info(H, W, Cl, n, p, warmup, cfg) -> dict:
