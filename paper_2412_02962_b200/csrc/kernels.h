@@ -31,6 +31,7 @@ struct GemmArgs {
   const float* temb = nullptr; int temb_ld = 0;   // temb[b*temb_ld + n]
   ActView res;                               // residual with out's geometry (base==nullptr: none)
   ActView out, out2; int n_split = 1 << 30;  // cols >= n_split -> out2[col - n_split]
+  float* ws = nullptr; size_t ws_elems = 0;  // split-K fp32 workspace (optional)
 };
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 

@@ -12,6 +12,7 @@
 // * SWIZZLE_128B K-major smem tiles, STAGES-deep mbarrier ring between TMA and MMA.
 #include <cuda.h>
 #include <cstdio>
+#include <cstdlib>
 #include "../common.cuh"
 #include "../kernels.h"
 #include "../sm100.cuh"
@@ -27,6 +28,8 @@ struct TcGemmParams {
   unsigned a_bytes;
   const float* bias; const float* temb; int temb_ld;
   ActView res, out, out2;
+  int splits, s_len;          // split-K: blockIdx.z covers k-steps [z*s_len, (z+1)*s_len)
+  float* ws;                  // [splits][M][N] fp32 partials (M = tokens in layout order)
 };
 
 template <int BN>
@@ -35,12 +38,15 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;   // 2 accumulators
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
 };
 
 template <int BN>
 __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__ TcGemmParams p) {
+  // Persistent: CTA c handles work units c, c + gridDim.x, ...; a unit = (m tile, n tile, k split).
+  // The smem ring (full/empty) runs continuously across units; two TMEM accumulators (tfull/tempty)
+  // let the epilogue of unit i overlap the main loop of unit i+1.
   using Cfg = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -48,14 +54,15 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
   uint64_t* empty = full + Cfg::STAGES;
-  uint64_t* tfull = empty + Cfg::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + Cfg::STAGES;     // [2]
+  uint64_t* tempty = tfull + 2;              // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&p.ma0); sm100::tma_prefetch(&p.ma1); sm100::tma_prefetch(&p.mb);
     for (int s = 0; s < Cfg::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    sm100::mbar_init(tfull, 1);
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 4); }
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -64,99 +71,146 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   sm100::fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // output tile -> (r0, b0, w0)
-  const int t = blockIdx.x;
-  int r0, b0, w0;
-  if (p.Bbox == 2) { r0 = t * p.Rbox; b0 = 0; w0 = 0; }
-  else { const int wt = t % p.nWt; const int tb = t / p.nWt; b0 = tb % p.B; r0 = tb / p.B; w0 = wt * p.Wbox; }
-  const int n0 = blockIdx.y * BN;
-  const int nsteps = p.taps * p.nkc;
+  const int n_tiles = p.N / BN;
+  const int units = p.m_tiles * n_tiles * p.splits;
+  const int nsteps_all = p.taps * p.nkc;
+  auto decode = [&](int u, int& r0, int& b0, int& w0, int& n0, int& z) {
+    const int mt = u % p.m_tiles;
+    const int rest = u / p.m_tiles;
+    n0 = (rest % n_tiles) * BN;
+    z = rest / n_tiles;
+    if (p.Bbox == 2) { r0 = mt * p.Rbox; b0 = 0; w0 = 0; }
+    else { const int wt = mt % p.nWt; const int tb = mt / p.nWt; b0 = tb % p.B; r0 = tb / p.B; w0 = wt * p.Wbox; }
+  };
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int s = 0; s < nsteps; ++s) {
-        const int st = s % Cfg::STAGES;
-        const uint32_t ph = (s / Cfg::STAGES) & 1;
-        sm100::mbar_wait(&empty[st], ph ^ 1);
-        const int tap = s / p.nkc, kc = s - tap * p.nkc;
-        const int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
-        sm100::mbar_arrive_expect_tx(&full[st], p.a_bytes + Cfg::B_BYTES);
-        if (kc < p.nk0)
-          sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma0, &full[st], kc * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
-        else
-          sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma1, &full[st], (kc - p.nk0) * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
-        sm100::tma_load_2d(sB + st * Cfg::B_BYTES, &p.mb, &full[st], s * 64, n0);
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int r0, b0, w0, n0, z;
+        decode(u, r0, b0, w0, n0, z);
+        const int s_begin = z * p.s_len, s_end = min(nsteps_all, s_begin + p.s_len);
+        for (int s = s_begin; s < s_end; ++s, ++it) {
+          const int st = it % Cfg::STAGES;
+          const uint32_t ph = (it / Cfg::STAGES) & 1;
+          sm100::mbar_wait(&empty[st], ph ^ 1);
+          const int tap = s / p.nkc, kc = s - tap * p.nkc;
+          const int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
+          sm100::mbar_arrive_expect_tx(&full[st], p.a_bytes + Cfg::B_BYTES);
+          if (kc < p.nk0)
+            sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma0, &full[st], kc * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
+          else
+            sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma1, &full[st], (kc - p.nk0) * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
+          sm100::tma_load_2d(sB + st * Cfg::B_BYTES, &p.mb, &full[st], s * 64, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = sm100::idesc_bf16(128, BN, 0, 0);
-      for (int s = 0; s < nsteps; ++s) {
-        const int st = s % Cfg::STAGES;
-        const uint32_t ph = (s / Cfg::STAGES) & 1;
-        sm100::mbar_wait(&full[st], ph);
+      int it = 0, tc = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++tc) {
+        int r0, b0, w0, n0, z;
+        decode(u, r0, b0, w0, n0, z);
+        const int s_begin = z * p.s_len, s_end = min(nsteps_all, s_begin + p.s_len);
+        const int a = tc & 1;
+        sm100::mbar_wait(&tempty[a], ((tc >> 1) & 1) ^ 1);
         sm100::fence_after();
-        const uint32_t a_base = sm100::smem_u32(sA + st * Cfg::A_BYTES);
-        const uint32_t b_base = sm100::smem_u32(sB + st * Cfg::B_BYTES);
+        const uint32_t d = tmem + a * BN;
+        for (int s = s_begin; s < s_end; ++s, ++it) {
+          const int st = it % Cfg::STAGES;
+          const uint32_t ph = (it / Cfg::STAGES) & 1;
+          sm100::mbar_wait(&full[st], ph);
+          sm100::fence_after();
+          const uint32_t a_base = sm100::smem_u32(sA + st * Cfg::A_BYTES);
+          const uint32_t b_base = sm100::smem_u32(sB + st * Cfg::B_BYTES);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t ad = sm100::sdesc_sw128(a_base + k * 32, 16, 1024);
-          const uint64_t bd = sm100::sdesc_sw128(b_base + k * 32, 16, 1024);
-          sm100::mma_bf16_ss(tmem, ad, bd, idesc, (s | k) != 0);
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = sm100::sdesc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = sm100::sdesc_sw128(b_base + k * 32, 16, 1024);
+            sm100::mma_bf16_ss(d, ad, bd, idesc, ((s - s_begin) | k) != 0);
+          }
+          sm100::mma_commit(&empty[st]);
         }
-        sm100::mma_commit(&empty[st]);
+        sm100::mma_commit(&tfull[a]);
       }
-      sm100::mma_commit(tfull);
     }
   } else {
     // epilogue: warp w reads TMEM lanes [32 (w%4), 32 (w%4) + 32)
     const int q = warp & 3;
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
-    const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
-    const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
-    sm100::mbar_wait(tfull, 0);
-    sm100::fence_after();
-    const bool second = n0 >= p.n_split;
-    const ActView& ov = second ? p.out2 : p.out;
-    const int ncol0 = second ? n0 - p.n_split : n0;
-    const long long orow = (((long long)r * ov.B + b) * ov.W + w) * ov.C + ncol0;
-    const long long rrow = p.res.base ? (((long long)r * p.res.B + b) * p.res.W + w) * p.res.C + n0 : 0;
+    int tc = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tc) {
+      int r0, b0, w0, n0, z;
+      decode(u, r0, b0, w0, n0, z);
+      const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
+      const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
+      const int a = tc & 1;
+      sm100::mbar_wait(&tfull[a], (tc >> 1) & 1);
+      sm100::fence_after();
+      const uint32_t tacc = tmem + a * BN + (uint32_t(q * 32) << 16);
+      const bool second = n0 >= p.n_split;
+      const ActView& ov = second ? p.out2 : p.out;
+      const int ncol0 = second ? n0 - p.n_split : n0;
+      const long long orow = (((long long)r * ov.B + b) * ov.W + w) * ov.C + ncol0;
+      const long long rrow = p.res.base ? (((long long)r * p.res.B + b) * p.res.W + w) * p.res.C + n0 : 0;
+      if (p.splits > 1) {
+        // split-K: raw fp32 partial tile -> workspace; gemm_splitk_finish applies the epilogue
+        const long long T = ((long long)r * p.B + b) * p.w_out + w;
+        float* wp = p.ws + ((long long)z * p.rows_out * p.B * p.w_out + T) * p.N + n0;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t v[32];
-      sm100::tmem_ld32(tmem + (uint32_t(q * 32) << 16) + c, v);
-      sm100::tmem_wait_ld();
-      if (!valid) continue;
-      float f[32];
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          sm100::tmem_ld32(tacc + c, v);
+          sm100::tmem_wait_ld();
+          if (!valid) continue;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-      if (p.bias) {
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(wp + c + 4 * j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                                    __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          sm100::tmem_ld32(tacc + c, v);
+          sm100::tmem_wait_ld();
+          if (!valid) continue;
+          float f[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n0 + c + i);
-      }
-      if (p.temb) {
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+          if (p.bias) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] += __ldg(p.temb + b * p.temb_ld + n0 + c + i);
-      }
-      if (p.res.base) {
-        float rv[8];
+            for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n0 + c + i);
+          }
+          if (p.temb) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          load8(reinterpret_cast<const bf16*>(p.res.base) + rrow + c + 8 * j, rv);
+            for (int i = 0; i < 32; ++i) f[i] += __ldg(p.temb + b * p.temb_ld + n0 + c + i);
+          }
+          if (p.res.base) {
+            float rv[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) f[8 * j + i] += rv[i];
+            for (int j = 0; j < 4; ++j) {
+              load8(reinterpret_cast<const bf16*>(p.res.base) + rrow + c + 8 * j, rv);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) f[8 * j + i] += rv[i];
+            }
+          }
+          if (ov.dtype == DT_BF16) {
+            bf16* po = reinterpret_cast<bf16*>(ov.base) + orow + c;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
+          } else {
+            float* po = reinterpret_cast<float*>(ov.base) + orow + c;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
+          }
         }
       }
-      if (ov.dtype == DT_BF16) {
-        bf16* po = reinterpret_cast<bf16*>(ov.base) + orow + c;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
-      } else {
-        float* po = reinterpret_cast<float*>(ov.base) + orow + c;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
-      }
+      sm100::fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[a]);
     }
   }
   sm100::fence_before();
@@ -236,8 +290,48 @@ bool gemm_tc_supported(const GemmArgs& g) {
 
 template <int BN>
 static void launch_bn(const TcGemmParams& p, cudaStream_t s) {
-  dim3 grid(p.m_tiles, p.N / BN);
-  gemm_tc_kernel<BN><<<grid, 192, TcCfg<BN>::SMEM, s>>>(p);
+  const int units = p.m_tiles * (p.N / BN) * p.splits;
+  gemm_tc_kernel<BN><<<units < 148 ? units : 148, 192, TcCfg<BN>::SMEM, s>>>(p);
+}
+
+// split-K epilogue: out[T][n] = sum_z ws[z][T][n] (fixed order) + bias + temb + residual
+__global__ void gemm_splitk_finish(const float* __restrict__ ws, int splits, long long M, int N, int W, int B,
+                                   const float* __restrict__ bias, const float* __restrict__ temb, int temb_ld,
+                                   ActView res, ActView out, ActView out2, int n_split) {
+  const int nv = N / 8;
+  const long long total = M * nv;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long T = i / nv;
+    const int n = (int)(i - T * nv) * 8;
+    float f[8], t[8];
+    load8(ws + T * N + n, f);
+    for (int z = 1; z < splits; ++z) {
+      load8(ws + ((long long)z * M + T) * N + n, t);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] += t[e];
+    }
+    const int b = (int)((T / W) % B);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (bias) f[e] += bias[n + e];
+      if (temb) f[e] += temb[b * temb_ld + n + e];
+    }
+    if (res.base) {
+      load8(reinterpret_cast<const bf16*>(res.base) + T * res.C + n, t);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] += t[e];
+    }
+    const bool second = n >= n_split;
+    const ActView& ov = second ? out2 : out;
+    const long long o = T * ov.C + (second ? n - n_split : n);
+    if (ov.dtype == DT_BF16) store8(reinterpret_cast<bf16*>(ov.base) + o, f);
+    else store8(reinterpret_cast<float*>(ov.base) + o, f);
+  }
+}
+
+static double wave_eff(long long ctas) {
+  const long long waves = (ctas + 147) / 148;
+  return (double)ctas / (double)(waves * 148);
 }
 
 void gemm_tc_init() {
@@ -268,11 +362,35 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (!encode_act(&p.ma0, g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_act(&p.ma1, g.a1.base ? g.a1 : g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN)) return false;
+  // split-K when the output tiles fill the 148 SMs poorly (small M: level 2, or n > 1 patches)
+  const int nsteps = p.taps * p.nkc;
+  const long long tiles = (long long)p.m_tiles * (g.N / BN);
+  const long long M = (long long)g.rows_out * g.B * g.w_out;
+  p.splits = 1; p.s_len = nsteps; p.ws = g.ws;
+  static const int splitk_env = getenv("PCPP_SPLITK") ? atoi(getenv("PCPP_SPLITK")) : 1;
+  if (splitk_env && g.ws && tiles < 148) {
+    double best = wave_eff(tiles);
+    for (int S = 2; S <= 8; ++S) {
+      if (nsteps / S < 8) break;
+      if ((size_t)S * M * g.N > g.ws_elems) break;
+      const double e = wave_eff(tiles * S) - 0.02 * (S - 1);
+      if (e > best + 0.05) { best = e; p.splits = S; }
+    }
+    p.s_len = (nsteps + p.splits - 1) / p.splits;
+    p.splits = (nsteps + p.s_len - 1) / p.s_len;
+  }
   switch (BN) {
     case 256: launch_bn<256>(p, s); break;
     case 160: launch_bn<160>(p, s); break;
     case 128: launch_bn<128>(p, s); break;
     default: launch_bn<64>(p, s); break;
+  }
+  if (p.splits > 1) {
+    const long long total = M * (g.N / 8);
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    gemm_splitk_finish<<<(unsigned)blocks, 256, 0, s>>>(p.ws, p.splits, M, g.N, g.w_out, g.B, g.bias, g.temb,
+                                                       g.temb_ld, g.res, g.out, g.out2, p.n_split);
   }
   return true;
 }

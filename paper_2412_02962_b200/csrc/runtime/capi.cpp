@@ -407,6 +407,14 @@ pcpp_status pcpp_op_conv(const void* x, int rows_in, int B, int W_in, int Cin, i
   g.w = w; g.wdtype = dt; g.N = Cout; g.bias = bias; g.temb = temb; g.temb_ld = Cout;
   g.out.base = y; g.out.rows = g.rows_out; g.out.B = B; g.out.W = g.w_out; g.out.C = Cout; g.out.dtype = dt;
   if (res) { g.res = g.out; g.res.base = const_cast<void*>(res); }
+  static float* ws = nullptr; static size_t ws_cap = 0;
+  const size_t need = 8ull * g.rows_out * B * g.w_out * Cout;
+  if (dt == DT_BF16 && need > ws_cap) {
+    if (ws) cudaFree(ws);
+    ws = nullptr; ws_cap = 0;
+    if (cudaMalloc(&ws, need * 4) == cudaSuccess) ws_cap = need;
+  }
+  g.ws = ws; g.ws_elems = ws_cap;
   launch_gemm_auto(g, impl == PCPP_KERNELS_AUTO, reinterpret_cast<cudaStream_t>(stream));
   CKS(cudaGetLastError());
   return PCPP_OK;

@@ -104,6 +104,16 @@ pcpp_status plan_allocate(Plan& P) {
   P.emb = (float*)galloc(2 * P.T * 4); P.hid = (float*)galloc(P.T * 4);
   P.tproj = (float*)galloc((size_t)2 * P.J * 4); P.cond = (float*)galloc(P.T * 4);
   P.taus = (int*)galloc(P.S * 4); P.coef = (double*)galloc(P.S * 4 * 8); P.k_dev = (int*)galloc(16);
+  if (P.dtype == DT_BF16) {       // split-K workspace: up to 8 fp32 partial copies of the largest GEMM output
+    size_t mx = 0;
+    for (const Op& o : P.ops)
+      if (o.k == OP_CONV || o.k == OP_GEMM) {
+        const TDesc& t = P.td[o.out];
+        mx = std::max(mx, (size_t)t.rows * B_CFG * t.W * (size_t)o.N);
+      }
+    P.ws_elems = std::min<size_t>(8 * mx, (size_t)1 << 28);
+    P.ws = (float*)galloc(P.ws_elems * 4);
+  }
   for (void* p : P.gallocs) if (!p) { set_error("cudaMalloc failed for global buffers"); return PCPP_ERR_OOM; }
   // DDIM schedule (reading D2): scaled_linear betas, 'leading' spacing, offset 1, final ab_prev = ab[0]
   std::vector<double> ab(1000);
@@ -447,6 +457,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           if (op.res >= 0) g.res = view(P, vr, op.res, par);
           g.out = o;
           if (op.out2 >= 0) { g.out2 = view(P, vr, op.out2, par); g.n_split = op.n_split; }
+          g.ws = P.ws; g.ws_elems = P.ws_elems;
           launch_gemm_tc_or_simt(P, g, s);
         }
         P.launches_per_step += nr;

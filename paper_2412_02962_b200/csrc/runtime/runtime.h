@@ -104,6 +104,7 @@ struct Plan {
   void* wmat = nullptr;  float* wf32 = nullptr;
   float* emb = nullptr; float* hid = nullptr; float* tproj = nullptr; float* cond = nullptr;
   int* taus = nullptr; double* coef = nullptr; int* k_dev = nullptr;
+  float* ws = nullptr; size_t ws_elems = 0;   // split-K workspace
   std::vector<void*> gallocs;
 
   // exchange descriptors: [sync][par] per exchange op index
