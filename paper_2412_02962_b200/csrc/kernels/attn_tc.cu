@@ -1,6 +1,6 @@
 // tcgen05 flash attention for partially conditioned attention (§3.3; Fig. 3), sm_100a.
 //
-// One CTA = 128 query tokens of one (batch b, head).  Q comes from the local fresh patch; the
+// One CTA = 2 x 128 query tokens of one (batch b, head) (two softmax warpgroups, ping-pong).  Q comes from the local fresh patch; the
 // key/value stream is the concatenation of up to three row sources [stale top band ; local fresh ;
 // stale bottom band] (Eq. 1; reading D13), each a [rows][B][W][2C] tensor read in place -- the
 // neighbour bands straight out of the receive buffers, no concat copy.
@@ -28,12 +28,13 @@ struct TcAttnParams {
 
 namespace {
 constexpr int TILE = 128 * 128;              // bytes of one 128-token x 64-dim bf16 tile
-constexpr int SM_Q = 0;
-constexpr int SM_K = TILE;                   // 2 stages
-constexpr int SM_V = 3 * TILE;               // 2 stages
-constexpr int SM_P = 5 * TILE;               // 2 x 16 KB atoms (keys 0-63, 64-127)
-constexpr int SM_BAR = 7 * TILE;
+constexpr int SM_Q = 0;                      // 2 query tiles (one per softmax warpgroup)
+constexpr int SM_K = 2 * TILE;               // 2 stages
+constexpr int SM_V = 4 * TILE;               // 2 stages
+constexpr int SM_P = 6 * TILE;               // 2 warpgroups x (2 x 16 KB atoms: keys 0-63, 64-127)
+constexpr int SM_BAR = 10 * TILE;
 constexpr int ATTN_SMEM = 1024 + SM_BAR + 256;
+constexpr int ATTN_THREADS = 320;            // warp 0 TMA, warp 1 MMA, warps 2-5 / 6-9 softmax WG 0 / 1
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -56,48 +57,57 @@ __device__ __forceinline__ void tile_coords(const TcAttnParams& p, int j, int& s
   w0 = (jj % p.nWt) * p.Wbox;
 }
 
-__global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__ TcAttnParams p) {
+// Two 128-query tiles of one (b, head) per CTA share every K/V tile.  The tensor core works on one
+// warpgroup's S / O while the other warpgroup runs its softmax (ping-pong), and each scheduler has
+// two softmax warps to interleave.
+__global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_constant__ TcAttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;      // [2]
-  uint64_t* kv_empty = bars + 3;     // [2]
-  uint64_t* s_full = bars + 5;       // [2]
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_full = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* kv_full = bars + 1;      // [2 stages]
+  uint64_t* kv_empty = bars + 3;     // [2 stages]
+  uint64_t* s_full = bars + 5;       // [2 wg]
+  uint64_t* p_full = bars + 7;       // [2 wg]
+  uint64_t* o_full = bars + 9;       // [2 wg]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
-  const int q_r0 = (qt / p.nWt) * p.Rbox, q_w0 = (qt % p.nWt) * p.Wbox;
+  const int head = blockIdx.y, b = blockIdx.z;
+  const int nqt = ((p.h + p.Rbox - 1) / p.Rbox) * p.nWt;
+  const int qt0 = 2 * blockIdx.x;
+  const int nwg = (qt0 + 1 < nqt) ? 2 : 1;          // query tiles in this CTA
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&p.mq);
     for (int s = 0; s < p.nsrc; ++s) sm100::tma_prefetch(&p.mkv[s]);
     sm100::mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) { sm100::mbar_init(&kv_full[i], 1); sm100::mbar_init(&kv_empty[i], 1); sm100::mbar_init(&s_full[i], 1); }
-    sm100::mbar_init(p_full, 128);
-    sm100::mbar_init(o_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&kv_full[i], 1); sm100::mbar_init(&kv_empty[i], 1);
+      sm100::mbar_init(&s_full[i], 1); sm100::mbar_init(&p_full[i], 128); sm100::mbar_init(&o_full[i], 1);
+    }
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<512>(tmem_slot);
   if (p.box_bytes < (unsigned)TILE) {
-    // partial key tiles: the rows past the TMA box must be finite (zero) for P V
-    uint4* z = reinterpret_cast<uint4*>(smem + SM_K);
-    for (int i = threadIdx.x; i < 4 * TILE / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    // partial tiles: rows past the TMA box must be finite (zero) for the MMAs
+    uint4* z = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < 6 * TILE / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
     sm100::fence_proxy_async_smem();
   }
   sm100::fence_before();
   __syncthreads();
   sm100::fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *tmem_slot;     // cols: S wg0 [0,128), S wg1 [128,256), O wg0 [256,320), O wg1 [320,384)
   const int nt = p.ntiles;
 
   if (warp == 0) {
     if (lane == 0) {
-      sm100::mbar_arrive_expect_tx(q_full, p.box_bytes);
-      sm100::tma_load_4d(smem + SM_Q, &p.mq, q_full, head * 64, q_w0, b, q_r0);
+      sm100::mbar_arrive_expect_tx(q_full, nwg * p.box_bytes);
+      for (int g = 0; g < nwg; ++g) {
+        const int qt = qt0 + g;
+        sm100::tma_load_4d(smem + SM_Q + g * TILE, &p.mq, q_full, head * 64, (qt % p.nWt) * p.Wbox, b, (qt / p.nWt) * p.Rbox);
+      }
       for (int j = 0; j < nt; ++j) {
         const int st = j & 1;
         sm100::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
@@ -112,121 +122,142 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
     if (lane == 0) {
       constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
-      const uint32_t q_base = sm100::smem_u32(smem + SM_Q);
-      const uint32_t p_base = sm100::smem_u32(smem + SM_P);
       sm100::mbar_wait(q_full, 0);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        sm100::mbar_wait(&kv_full[st], (j >> 1) & 1);
-        sm100::fence_after();
-        const uint32_t k_base = sm100::smem_u32(smem + SM_K + st * TILE);
+      auto issue_s = [&](int g, int j) {
+        const uint32_t q_base = sm100::smem_u32(smem + SM_Q + g * TILE);
+        const uint32_t k_base = sm100::smem_u32(smem + SM_K + (j & 1) * TILE);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          sm100::mma_bf16_ss(tmem + st * 128, sm100::sdesc_sw128(q_base + k * 32, 16, 1024),
+          sm100::mma_bf16_ss(tmem + g * 128, sm100::sdesc_sw128(q_base + k * 32, 16, 1024),
                              sm100::sdesc_sw128(k_base + k * 32, 16, 1024), id_s, k != 0);
-        sm100::mma_commit(&s_full[st]);
+        sm100::mma_commit(&s_full[g]);
       };
-      if (nt > 0) issue_s(0);
-      for (int j = 0; j < nt; ++j) {
-        const int st = j & 1;
-        if (j + 1 < nt) issue_s(j + 1);
-        sm100::mbar_wait(p_full, j & 1);
-        sm100::fence_after();
-        const uint32_t v_base = sm100::smem_u32(smem + SM_V + st * TILE);
+      auto issue_o = [&](int g, int j) {
+        const uint32_t p_base = sm100::smem_u32(smem + SM_P + g * 2 * TILE);
+        const uint32_t v_base = sm100::smem_u32(smem + SM_V + (j & 1) * TILE);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          sm100::mma_bf16_ss(tmem + 256, sm100::sdesc_sw128(p_base + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
+          sm100::mma_bf16_ss(tmem + 256 + g * 64, sm100::sdesc_sw128(p_base + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
                              sm100::sdesc_sw128(v_base + k * 2048, 16384, 1024), id_o, (j | k) != 0);
-        sm100::mma_commit(o_full);
-        sm100::mma_commit(&kv_empty[st]);
+        sm100::mma_commit(&o_full[g]);
+      };
+      if (nt > 0) {
+        sm100::mbar_wait(&kv_full[0], 0);
+        sm100::fence_after();
+        for (int g = 0; g < nwg; ++g) issue_s(g, 0);
+      }
+      for (int j = 0; j < nt; ++j) {
+        for (int g = 0; g < nwg; ++g) {
+          sm100::mbar_wait(&p_full[g], j & 1);      // softmax g has read S_g(j) and written P_g(j)
+          sm100::fence_after();
+          issue_o(g, j);
+          if (g == nwg - 1) sm100::mma_commit(&kv_empty[j & 1]);   // K_j, V_j free once both O MMAs finish
+          if (j + 1 < nt) {
+            if (g == 0) { sm100::mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1); sm100::fence_after(); }
+            issue_s(g, j + 1);
+          }
+        }
       }
     }
   } else {
-    // softmax warpgroup: TMEM lane quarter = warp % 4, thread = query row.  O accumulates in
-    // TMEM across key tiles; the running max is only raised (and O, l rescaled) when a tile's max
-    // exceeds it by more than 2^8, so most tiles need no rescale (p <= 256 stays exact in fp32).
-    const int qw = warp & 3;
-    const int row = qw * 32 + lane;
-    const uint32_t trow = tmem + (uint32_t(qw * 32) << 16);
-    const float sl2 = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
-    float m = -INFINITY, l = 0.f;
-    uint8_t* P = smem + SM_P;
-    for (int j = 0; j < nt; ++j) {
-      const int st = j & 1;
-      int s, r0, w0;
-      tile_coords(p, j, s, r0, w0);
-      const int nvr = min(p.Rbox, p.rows[s] - r0);         // valid rows in this key tile
-      const int nvw = min(p.Wbox, p.W - w0);               // valid cols
-      // keys are a contiguous valid prefix: Rbox > 1 only when Wbox == W (full rows)
-      const int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;
-      sm100::mbar_wait(&s_full[st], (j >> 1) & 1);
-      sm100::fence_after();
-      float sv[128];
-#pragma unroll
-      for (int c = 0; c < 128; c += 32) sm100::tmem_ld32(trow + st * 128 + c, reinterpret_cast<uint32_t*>(sv + c));
-      sm100::tmem_wait_ld();
-      float mx = -INFINITY;
-      if (nvalid >= 128) {
-#pragma unroll
-        for (int i = 0; i < 128; ++i) mx = fmaxf(mx, sv[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 128; ++i) { if (i >= nvalid) sv[i] = -INFINITY; mx = fmaxf(mx, sv[i]); }
-      }
-      mx *= sl2;
-      const bool raise = mx > m + 8.0f;
-      const float m_new = raise ? mx : m;
-      const float alpha = raise ? (m == -INFINITY ? 0.f : fast_exp2(m - m_new)) : 1.f;
-      // O_{j-1} must be complete before P_j overwrites P_{j-1} and before O is rescaled
-      if (j > 0) {
-        sm100::mbar_wait(o_full, (j - 1) & 1);
+    // softmax warpgroup g: TMEM lane quarter = warp % 4, thread = query row.  O accumulates in TMEM;
+    // the running max is only raised (O, l rescaled) when a tile's max exceeds it by > 2^8.
+    const int g = (warp - 2) >> 2;
+    if (g < nwg) {
+      const int qw = warp & 3;
+      const int row = qw * 32 + lane;
+      const uint32_t trow = tmem + (uint32_t(qw * 32) << 16);
+      const uint32_t t_s = trow + g * 128, t_o = trow + 256 + g * 64;
+      const float sl2 = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
+      float m = -INFINITY, l = 0.f;
+      uint8_t* P = smem + SM_P + g * 2 * TILE;
+      for (int j = 0; j < nt; ++j) {
+        int s, r0, w0;
+        tile_coords(p, j, s, r0, w0);
+        const int nvr = min(p.Rbox, p.rows[s] - r0);
+        const int nvw = min(p.Wbox, p.W - w0);
+        const int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;   // valid keys form a prefix
+        sm100::mbar_wait(&s_full[g], j & 1);
         sm100::fence_after();
-        if (__any_sync(0xffffffffu, raise)) {
+        // pass 1: row max (S stays in TMEM; two cheap passes keep registers below the 320-thread cap)
+        float mx = -INFINITY;
 #pragma unroll
-          for (int c = 0; c < 64; c += 16) {
-            uint32_t v[16];
-            sm100::tmem_ld16(trow + 256 + c, v);
-            sm100::tmem_wait_ld();
-            uint32_t o16[16];
+        for (int c = 0; c < 128; c += 32) {
+          float sv[32];
+          sm100::tmem_ld32(t_s + c, reinterpret_cast<uint32_t*>(sv));
+          sm100::tmem_wait_ld();
+          if (nvalid >= 128) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o16[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-            sm100::tmem_st16(trow + 256 + c, o16);
+            for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(sv[i], sv[i + 1]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mx = (c + i < nvalid) ? fmaxf(mx, sv[i]) : mx;
           }
-          sm100::tmem_wait_st();
         }
+        mx *= sl2;
+        const bool raise = mx > m + 8.0f;
+        const float m_new = raise ? mx : m;
+        const float alpha = raise ? (m == -INFINITY ? 0.f : fast_exp2(m - m_new)) : 1.f;
+        if (j > 0) {                          // O(j-1) done: P may be overwritten, O may be rescaled
+          sm100::mbar_wait(&o_full[g], (j - 1) & 1);
+          sm100::fence_after();
+          if (__any_sync(0xffffffffu, raise)) {
+#pragma unroll
+            for (int c = 0; c < 64; c += 16) {
+              uint32_t v[16];
+              sm100::tmem_ld16(t_o + c, v);
+              sm100::tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+              sm100::tmem_st16(t_o + c, v);
+            }
+            sm100::tmem_wait_st();
+          }
+        }
+        // pass 2: p = exp2(s * scale - m) -> bf16 P (K-major SW128 smem), row sum
+        float ls = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) {
+          float sv[32];
+          sm100::tmem_ld32(t_s + c, reinterpret_cast<uint32_t*>(sv));
+          sm100::tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float pv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float e = fast_exp2(fmaf(sv[8 * u + i], sl2, -m_new));
+              pv[i] = (nvalid >= 128 || c + 8 * u + i < nvalid) ? e : 0.f;
+              ls += pv[i];
+            }
+            const int key0 = c + 8 * u, atom = key0 >> 6, chunk = (key0 & 63) >> 3;
+            store8(reinterpret_cast<bf16*>(P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4)), pv);
+          }
+        }
+        l = l * alpha + ls;
+        m = m_new;
+        sm100::fence_proxy_async_smem();
+        sm100::fence_before();
+        sm100::mbar_arrive(&p_full[g]);
       }
-      float ls = 0.f;
-#pragma unroll
-      for (int c = 0; c < 128; c += 8) {
-        float pv[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) { pv[i] = fast_exp2(fmaf(sv[c + i], sl2, -m_new)); ls += pv[i]; }
-        const int atom = c >> 6, chunk = (c & 63) >> 3;
-        store8(reinterpret_cast<bf16*>(P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4)), pv);
+      if (nt > 0) {
+        sm100::mbar_wait(&o_full[g], (nt - 1) & 1);
+        sm100::fence_after();
       }
-      l = l * alpha + ls;
-      m = m_new;
-      sm100::fence_proxy_async_smem();
-      sm100::fence_before();
-      sm100::mbar_arrive(p_full);
-    }
-    if (nt > 0) {
-      sm100::mbar_wait(o_full, (nt - 1) & 1);
-      sm100::fence_after();
-    }
-    float acc[64];
+      float acc[64];
 #pragma unroll
-    for (int c = 0; c < 64; c += 32) sm100::tmem_ld32(trow + 256 + c, reinterpret_cast<uint32_t*>(acc + c));
-    sm100::tmem_wait_ld();
-    const int ri = row / p.Wbox, wi = row % p.Wbox;
-    const int r = q_r0 + ri, w = q_w0 + wi;
-    if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
-      const float inv = 1.f / l;
+      for (int c = 0; c < 64; c += 32) sm100::tmem_ld32(t_o + c, reinterpret_cast<uint32_t*>(acc + c));
+      sm100::tmem_wait_ld();
+      const int qt = qt0 + g;
+      const int r = (qt / p.nWt) * p.Rbox + row / p.Wbox, w = (qt % p.nWt) * p.Wbox + row % p.Wbox;
+      if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
+        const float inv = 1.f / l;
 #pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] *= inv;
-      bf16* o = reinterpret_cast<bf16*>(p.out) + (((long long)r * p.B + b) * p.W + w) * p.C + head * 64;
+        for (int i = 0; i < 64; ++i) acc[i] *= inv;
+        bf16* o = reinterpret_cast<bf16*>(p.out) + (((long long)r * p.B + b) * p.W + w) * p.C + head * 64;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) store8(o + 8 * u, acc + 8 * u);
+        for (int u = 0; u < 8; ++u) store8(o + 8 * u, acc + 8 * u);
+      }
     }
   }
   sm100::fence_before();
@@ -282,8 +313,8 @@ bool launch_attn_tc(const AttnArgs& a, cudaStream_t s) {
   }
   for (int i = p.nsrc; i < 3; ++i) p.mkv[i] = p.mkv[0];
   const int qtiles = ((a.h + p.Rbox - 1) / p.Rbox) * p.nWt;
-  dim3 grid(qtiles, a.C / 64, a.B);
-  attn_tc_kernel<<<grid, 192, ATTN_SMEM, s>>>(p);
+  dim3 grid((qtiles + 1) / 2, a.C / 64, a.B);
+  attn_tc_kernel<<<grid, ATTN_THREADS, ATTN_SMEM, s>>>(p);
   return true;
 }
 
