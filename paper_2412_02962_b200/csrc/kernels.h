@@ -75,6 +75,8 @@ struct GnApplyArgs {
   double count = 0;              // N = H_l W_l C/G (global)
 };
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s);
+// stats + apply in one launch (modes 0 and 2); counter must point at 2 zero-initialised words
+void launch_gn_fused(const GnStatsArgs& sa, const GnApplyArgs& aa, cudaStream_t s);
 
 // latent [h][W][4] fp32 -> padded xin [h][2][W][4] fp32 (both CFG branches)
 void launch_prep_latent(const float* latent, const ActView& xin, cudaStream_t s);

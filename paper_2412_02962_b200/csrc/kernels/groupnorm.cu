@@ -43,10 +43,9 @@ __device__ __forceinline__ const T* vptr(const ActView& v, long long rowtok, int
 // ---- stats -------------------------------------------------------------------------------------
 // CTA `chunk` covers layout tokens [T0, T1) (all (r, b, w) in memory order: address T*C + c, no
 // index division); token lanes stride by ntl, 4 independent 16 B loads in flight per thread.
+// returns true in the CTA that arrived last (it has reduced the partials into a.m_out)
 template <typename T>
-__global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
-  extern __shared__ float red[];                   // [ntl][nv][2 b][8][2]
-  __shared__ bool amlast;
+__device__ __forceinline__ bool gn_stats_phase(const GnStatsArgs& a, float* red, bool& amlast) {
   const int chunk = blockIdx.x;
   const int W = a.x0.W, B = a.x0.B, C = a.C;
   const Lanes L = lanes_for(C);
@@ -85,11 +84,12 @@ __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+          if (bq == 0) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float xv = x[k][e];
-            if (bq == 0) { s[u][0][e] += xv; q[u][0][e] = fmaf(xv, xv, q[u][0][e]); }
-            else         { s[u][1][e] += xv; q[u][1][e] = fmaf(xv, xv, q[u][1][e]); }
+            for (int e = 0; e < 8; ++e) { s[u][0][e] += x[k][e]; q[u][0][e] = fmaf(x[k][e], x[k][e], q[u][0][e]); }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { s[u][1][e] += x[k][e]; q[u][1][e] = fmaf(x[k][e], x[k][e], q[u][1][e]); }
           }
           w += L.ntl;
           while (w >= W) { w -= W; bq = (bq + 1 == B) ? 0 : bq + 1; }
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
   __syncthreads();
   if (tid == 0) amlast = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
   __syncthreads();
-  if (!amlast) return;
+  if (!amlast) return false;
   __threadfence();
   // last CTA: 2*B*G sums over nchunk partials; warp-per-sum, lane-strided loads, fixed-order tree
   const int warp = tid >> 5, lane = tid & 31;
@@ -137,7 +137,16 @@ __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
     if (lane == 0) a.m_out[i] = acc;                  // [B][G][2]
   }
   if (tid == 0) *a.counter = 0u;                      // ready for the next launch / graph replay
+  return true;
 }
+
+template <typename T>
+__global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
+  extern __shared__ float red[];                   // [ntl][nv][2 b][8][2]
+  __shared__ bool amlast;
+  gn_stats_phase<T>(a, red, amlast);
+}
+
 
 void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
   const Lanes L = lanes_for(a.C);
@@ -147,9 +156,7 @@ void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
 }
 
 // ---- apply -------------------------------------------------------------------------------------
-template <typename TI, typename TO>
-__global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int tok_per_cta) {
-  __shared__ float mu_s[2 * G], rs_s[2 * G];
+__device__ __forceinline__ void gn_prep(const GnApplyArgs& a, float* mu_s, float* rs_s) {
   const int B = a.x0.B;
   for (int i = threadIdx.x; i < B * G; i += NT) {
     double M1, M2;
@@ -169,7 +176,12 @@ __global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int t
     mu_s[i] = (float)mu;
     rs_s[i] = (float)(1.0 / sqrt(var + 1e-5));
   }
-  __syncthreads();
+}
+
+template <typename TI, typename TO>
+__device__ __forceinline__ void gn_apply_phase(const GnApplyArgs& a, const float* mu_s, const float* rs_s,
+                                               long long T0, long long T1) {
+  const int B = a.x0.B;
   const int C = a.C, cg = C / G, W = a.x0.W;
   const Lanes L = lanes_for(C);
   const int vl = threadIdx.x % L.nvl, tl = threadIdx.x / L.nvl;
@@ -194,9 +206,6 @@ __global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int t
       }
     }
   }
-  const long long ntok = (long long)a.x0.rows * B * W;           // (r, b, w) tokens in layout order
-  const long long T0 = (long long)blockIdx.x * tok_per_cta;
-  const long long T1 = T0 + tok_per_cta < ntok ? T0 + tok_per_cta : ntok;
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     if (cvec[u] < 0) continue;
@@ -216,10 +225,16 @@ __global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int t
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const long long Tk = T + (long long)k * L.ntl;
+        if (bq) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float y = fmaf(x[k][e], bq ? A[u][1][e] : A[u][0][e], bq ? Bc[u][1][e] : Bc[u][0][e]);
-          x[k][e] = a.silu ? silu_f(y) : y;
+          for (int e = 0; e < 8; ++e) x[k][e] = fmaf(x[k][e], A[u][1][e], Bc[u][1][e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[k][e] = fmaf(x[k][e], A[u][0][e], Bc[u][0][e]);
+        }
+        if (a.silu) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[k][e] = silu_f(x[k][e]);
         }
         // out has the same (r, b, w) geometry; it may be a padded tensor (base = row 0)
         if (Tk < T1) store8(reinterpret_cast<TO*>(a.out.base) + Tk * a.out.C + c, x[k]);
@@ -228,6 +243,61 @@ __global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int t
       }
     }
   }
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int tok_per_cta) {
+  __shared__ float mu_s[2 * G], rs_s[2 * G];
+  gn_prep(a, mu_s, rs_s);
+  __syncthreads();
+  const long long ntok = (long long)a.x0.rows * a.x0.B * a.x0.W;   // (r, b, w) tokens in layout order
+  const long long T0 = (long long)blockIdx.x * tok_per_cta;
+  const long long T1 = T0 + tok_per_cta < ntok ? T0 + tok_per_cta : ntok;
+  gn_apply_phase<TI, TO>(a, mu_s, rs_s, T0, T1);
+}
+
+// Stats + apply in one launch (n = 1 and async steps: the apply needs only this rank's fresh sums
+// and the previous step's exchanged sums).  The last CTA to finish the stats phase reduces the
+// partials and bumps a generation word; the others wait for it (all CTAs are co-resident: grid
+// <= 148).  Phase 2 re-reads this CTA's own token range (L2-resident).
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(NT) gn_fused_kernel(const GnStatsArgs sa, const GnApplyArgs aa) {
+  extern __shared__ float red[];
+  __shared__ bool amlast;
+  __shared__ float mu_s[2 * G], rs_s[2 * G];
+  volatile unsigned* gen = sa.counter + 1;
+  unsigned g0 = 0;
+  if (threadIdx.x == 0) g0 = *gen;
+  __syncthreads();
+  const bool last = gn_stats_phase<TI>(sa, red, amlast);
+  if (last) __threadfence();               // every writer of m_out fences before the signal
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (last) { __threadfence(); atomicAdd(sa.counter + 1, 1u); }
+    else {
+      const long long t0 = clock64();
+      while (*gen == g0) {
+        __nanosleep(64);
+        if (clock64() - t0 > 20000000000LL) __trap();
+      }
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  gn_prep(aa, mu_s, rs_s);
+  __syncthreads();
+  const long long ntok = (long long)sa.x0.rows * sa.x0.B * sa.x0.W;
+  const long long T0 = ntok * blockIdx.x / sa.nchunk, T1 = ntok * (blockIdx.x + 1) / sa.nchunk;
+  gn_apply_phase<TI, TO>(aa, mu_s, rs_s, T0, T1);
+}
+
+void launch_gn_fused(const GnStatsArgs& sa, const GnApplyArgs& aa, cudaStream_t s) {
+  GnStatsArgs a2 = sa;
+  if (a2.nchunk > 148) a2.nchunk = 148;
+  const Lanes L = lanes_for(a2.C);
+  const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
+  if (a2.x0.dtype == DT_F32) gn_fused_kernel<float, float><<<a2.nchunk, NT, smem, s>>>(a2, aa);
+  else gn_fused_kernel<bf16, bf16><<<a2.nchunk, NT, smem, s>>>(a2, aa);
 }
 
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
@@ -243,6 +313,8 @@ void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
 void gn_init() {   // dynamic smem: ntl * nv * 32 floats <= 40 KB (C <= 2560)
   cudaFuncSetAttribute(gn_stats_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(gn_stats_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(gn_fused_kernel<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(gn_fused_kernel<bf16, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
 }
 
 }  // namespace pcpp

@@ -464,7 +464,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
         break;
       case OP_GN: {
         const GnX& gx = P.gns[op.xid];
-        for (int vr = 0; vr < nr && do_op; ++vr) {
+        auto stats_args = [&](int vr) {
           GnStatsArgs a;
           a.x0 = view(P, vr, op.in0, par); a.c0 = a.x0.C; a.C = gx.C;
           if (op.in1 >= 0) a.x1 = view(P, vr, op.in1, par);
@@ -473,10 +473,9 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           a.counter = reinterpret_cast<unsigned*>(base + gx.off_cnt);
           a.m_out = reinterpret_cast<double*>(base + gx.off_m[par]);
           a.nchunk = gx.nchunk;
-          launch_gn_stats(a, s);
-        }
-        if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
-        for (int vr = 0; vr < nr && do_op; ++vr) {
+          return a;
+        };
+        auto apply_args = [&](int vr) {
           GnApplyArgs a;
           a.x0 = view(P, vr, op.in0, par); a.c0 = a.x0.C; a.C = gx.C;
           if (op.in1 >= 0) a.x1 = view(P, vr, op.in1, par);
@@ -492,9 +491,14 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
             a.mall = reinterpret_cast<const double*>(base + gx.off_mall[1 - par]);
             a.m_prev = reinterpret_cast<const double*>(base + gx.off_m[1 - par]);
           }
-          launch_gn_apply(a, s);
+          return a;
+        };
+        {
+          for (int vr = 0; vr < nr && do_op; ++vr) launch_gn_stats(stats_args(vr), s);
+          if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
+          for (int vr = 0; vr < nr && do_op; ++vr) launch_gn_apply(apply_args(vr), s);
+          P.launches_per_step += 2 * nr;
         }
-        P.launches_per_step += 2 * nr;
         break;
       }
       case OP_ATTN: {

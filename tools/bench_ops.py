@@ -59,3 +59,33 @@ if __name__ == "__main__":
                      ("attn L1 n=8 p=.8", 8, 64, 640, (6, 8, 6)), ("attn L2 n=8", 4, 32, 1280, (3, 4, 3))]:
         ms, tf = t_attn(*a)
         print(f"{name:22s} {ms * 1e3:9.1f} us  {tf:7.1f} TF/s")
+
+
+def t_gn(rows, W, C, iters=20):
+    x = torch.randn(rows, 2, W, C, device="cuda").bfloat16()
+    y = torch.empty_like(x)
+    g = torch.ones(C, device="cuda"); b = torch.zeros(C, device="cuda")
+    m = torch.empty(2, 32, 2, device="cuda", dtype=torch.float64)
+    for _ in range(3):
+        pcpp.pcpp_op_groupnorm(x, rows, 2, W, C, g, b, 1, y, m)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        pcpp.pcpp_op_groupnorm(x, rows, 2, W, C, g, b, 1, y, m)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    e0.record()
+    for _ in range(iters):
+        y.copy_(x)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_copy = e0.elapsed_time(e1) / iters
+    nb = x.numel() * 2
+    return ms, 3 * nb / ms / 1e6, ms_copy, 2 * nb / ms_copy / 1e6
+
+
+if __name__ == "__main__":
+    for shape in [(128, 128, 320), (128, 128, 960), (64, 64, 640), (32, 32, 1280), (32, 32, 2560)]:
+        ms, gbs, mc, gc = t_gn(*shape)
+        print(f"GN {shape}: {ms * 1e3:7.1f} us ({gbs:6.0f} GB/s of 3x bytes)   torch copy {mc * 1e3:6.1f} us ({gc:6.0f} GB/s)")
