@@ -28,12 +28,14 @@ struct TcAttnParams {
 
 namespace {
 constexpr int TILE = 128 * 128;              // bytes of one 128-token x 64-dim bf16 tile
+constexpr int KST = 3;                       // K/V pipeline stages
 constexpr int SM_Q = 0;                      // 2 query tiles (one per softmax warpgroup)
-constexpr int SM_K = 2 * TILE;               // 2 stages
-constexpr int SM_V = 4 * TILE;               // 2 stages
-constexpr int SM_P = 6 * TILE;               // 2 warpgroups x (2 x 16 KB atoms: keys 0-63, 64-127)
-constexpr int SM_BAR = 10 * TILE;
+constexpr int SM_K = 2 * TILE;               // KST stages
+constexpr int SM_V = SM_K + KST * TILE;      // KST stages
+constexpr int SM_P = SM_V + KST * TILE;      // 2 warpgroups x (2 x 16 KB atoms: keys 0-63, 64-127)
+constexpr int SM_BAR = SM_P + 4 * TILE;
 constexpr int ATTN_SMEM = 1024 + SM_BAR + 256;
+static_assert(ATTN_SMEM <= 227 * 1024, "attention smem");
 constexpr int ATTN_THREADS = 320;            // warp 0 TMA, warp 1 MMA, warps 2-5 / 6-9 softmax WG 0 / 1
 }
 
@@ -65,12 +67,13 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;      // [2 stages]
-  uint64_t* kv_empty = bars + 3;     // [2 stages]
-  uint64_t* s_full = bars + 5;       // [2 wg]
-  uint64_t* p_full = bars + 7;       // [2 wg]
-  uint64_t* o_full = bars + 9;       // [2 wg]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* kv_full = bars + 1;      // [KST]
+  uint64_t* kv_empty = bars + 1 + KST;   // [KST]
+  uint64_t* s_full = bars + 1 + 2 * KST; // [2 wg]
+  uint64_t* p_full = s_full + 2;     // [2 wg]
+  uint64_t* o_full = s_full + 4;     // [2 wg]
+  uint64_t* s_free = s_full + 6;     // [2 wg]: softmax has finished reading S (next S may be issued)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y, b = blockIdx.z;
@@ -82,9 +85,10 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
     sm100::tma_prefetch(&p.mq);
     for (int s = 0; s < p.nsrc; ++s) sm100::tma_prefetch(&p.mkv[s]);
     sm100::mbar_init(q_full, 1);
+    for (int i = 0; i < KST; ++i) { sm100::mbar_init(&kv_full[i], 1); sm100::mbar_init(&kv_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
-      sm100::mbar_init(&kv_full[i], 1); sm100::mbar_init(&kv_empty[i], 1);
       sm100::mbar_init(&s_full[i], 1); sm100::mbar_init(&p_full[i], 128); sm100::mbar_init(&o_full[i], 1);
+      sm100::mbar_init(&s_free[i], 128);
     }
     sm100::fence_barrier_init();
   }
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
   if (p.box_bytes < (unsigned)TILE) {
     // partial tiles: rows past the TMA box must be finite (zero) for the MMAs
     uint4* z = reinterpret_cast<uint4*>(smem);
-    for (int i = threadIdx.x; i < 6 * TILE / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < SM_P / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
     sm100::fence_proxy_async_smem();
   }
   sm100::fence_before();
@@ -109,8 +113,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         sm100::tma_load_4d(smem + SM_Q + g * TILE, &p.mq, q_full, head * 64, (qt % p.nWt) * p.Wbox, b, (qt / p.nWt) * p.Rbox);
       }
       for (int j = 0; j < nt; ++j) {
-        const int st = j & 1;
-        sm100::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % KST;
+        sm100::mbar_wait(&kv_empty[st], ((j / KST) & 1) ^ 1);
         int s, r0, w0;
         tile_coords(p, j, s, r0, w0);
         sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * p.box_bytes);
@@ -125,7 +129,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
       sm100::mbar_wait(q_full, 0);
       auto issue_s = [&](int g, int j) {
         const uint32_t q_base = sm100::smem_u32(smem + SM_Q + g * TILE);
-        const uint32_t k_base = sm100::smem_u32(smem + SM_K + (j & 1) * TILE);
+        const uint32_t k_base = sm100::smem_u32(smem + SM_K + (j % KST) * TILE);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           sm100::mma_bf16_ss(tmem + g * 128, sm100::sdesc_sw128(q_base + k * 32, 16, 1024),
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
       };
       auto issue_o = [&](int g, int j) {
         const uint32_t p_base = sm100::smem_u32(smem + SM_P + g * 2 * TILE);
-        const uint32_t v_base = sm100::smem_u32(smem + SM_V + (j & 1) * TILE);
+        const uint32_t v_base = sm100::smem_u32(smem + SM_V + (j % KST) * TILE);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           sm100::mma_bf16_ss(tmem + 256 + g * 64, sm100::sdesc_sw128(p_base + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
@@ -148,14 +152,16 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
       }
       for (int j = 0; j < nt; ++j) {
         for (int g = 0; g < nwg; ++g) {
-          sm100::mbar_wait(&p_full[g], j & 1);      // softmax g has read S_g(j) and written P_g(j)
-          sm100::fence_after();
-          issue_o(g, j);
-          if (g == nwg - 1) sm100::mma_commit(&kv_empty[j & 1]);   // K_j, V_j free once both O MMAs finish
-          if (j + 1 < nt) {
-            if (g == 0) { sm100::mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1); sm100::fence_after(); }
+          if (j + 1 < nt) {                          // S_g(j+1) as soon as softmax g is done reading S_g(j)
+            sm100::mbar_wait(&s_free[g], j & 1);
+            if (g == 0) sm100::mbar_wait(&kv_full[(j + 1) % KST], ((j + 1) / KST) & 1);
+            sm100::fence_after();
             issue_s(g, j + 1);
           }
+          sm100::mbar_wait(&p_full[g], j & 1);      // P_g(j) written
+          sm100::fence_after();
+          issue_o(g, j);
+          if (g == nwg - 1) sm100::mma_commit(&kv_empty[j % KST]);   // K_j, V_j free once both O MMAs finish
         }
       }
     }
@@ -179,21 +185,32 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         const int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;   // valid keys form a prefix
         sm100::mbar_wait(&s_full[g], j & 1);
         sm100::fence_after();
-        // pass 1: row max (S stays in TMEM; two cheap passes keep registers below the 320-thread cap)
+        // pass 1: row max.  Columns 64-127 stay in registers; 0-63 are re-read in pass 2, after
+        // which S is released (s_free) so the MMA warp can start S(j+1) under the exponentials.
+        float hi[64], lo[32];
+        sm100::tmem_ld32(t_s + 64, reinterpret_cast<uint32_t*>(hi));
+        sm100::tmem_ld32(t_s + 96, reinterpret_cast<uint32_t*>(hi + 32));
+        sm100::tmem_ld32(t_s + 0, reinterpret_cast<uint32_t*>(lo));
+        sm100::tmem_wait_ld();
+        if (nvalid < 128) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) if (64 + i >= nvalid) hi[i] = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) if (i >= nvalid) lo[i] = -INFINITY;
+        }
         float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 128; c += 32) {
-          float sv[32];
-          sm100::tmem_ld32(t_s + c, reinterpret_cast<uint32_t*>(sv));
-          sm100::tmem_wait_ld();
-          if (nvalid >= 128) {
+        for (int i = 0; i < 64; i += 2) mx = fmaxf(mx, fmaxf(hi[i], hi[i + 1]));
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(sv[i], sv[i + 1]));
-          } else {
+        for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(lo[i], lo[i + 1]));
+        sm100::tmem_ld32(t_s + 32, reinterpret_cast<uint32_t*>(lo));
+        sm100::tmem_wait_ld();
+        if (nvalid < 128) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) mx = (c + i < nvalid) ? fmaxf(mx, sv[i]) : mx;
-          }
+          for (int i = 0; i < 32; ++i) if (32 + i >= nvalid) lo[i] = -INFINITY;
         }
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(lo[i], lo[i + 1]));
         mx *= sl2;
         const bool raise = mx > m + 8.0f;
         const float m_new = raise ? mx : m;
@@ -216,24 +233,27 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         }
         // pass 2: p = exp2(s * scale - m) -> bf16 P (K-major SW128 smem), row sum
         float ls = 0.f;
+        auto emit8 = [&](const float* sv, int key0) {
+          float pv[8];
 #pragma unroll
-        for (int c = 0; c < 128; c += 32) {
-          float sv[32];
-          sm100::tmem_ld32(t_s + c, reinterpret_cast<uint32_t*>(sv));
-          sm100::tmem_wait_ld();
+          for (int i = 0; i < 8; ++i) { pv[i] = fast_exp2(fmaf(sv[i], sl2, -m_new)); ls += pv[i]; }
+          const int atom = key0 >> 6, chunk = (key0 & 63) >> 3;
+          store8(reinterpret_cast<bf16*>(P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4)), pv);
+        };
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float pv[8];
+        for (int u = 0; u < 4; ++u) emit8(lo + 8 * u, 32 + 8 * u);           // cols 32-63 (still in lo)
+        sm100::tmem_ld32(t_s + 0, reinterpret_cast<uint32_t*>(lo));
+        sm100::tmem_wait_ld();
+        sm100::fence_before();
+        sm100::mbar_arrive(&s_free[g]);                                        // S(j) no longer read
+        if (nvalid < 128) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float e = fast_exp2(fmaf(sv[8 * u + i], sl2, -m_new));
-              pv[i] = (nvalid >= 128 || c + 8 * u + i < nvalid) ? e : 0.f;
-              ls += pv[i];
-            }
-            const int key0 = c + 8 * u, atom = key0 >> 6, chunk = (key0 & 63) >> 3;
-            store8(reinterpret_cast<bf16*>(P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4)), pv);
-          }
+          for (int i = 0; i < 32; ++i) if (i >= nvalid) lo[i] = -INFINITY;
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) emit8(lo + 8 * u, 8 * u);                 // cols 0-31
+#pragma unroll
+        for (int u = 0; u < 8; ++u) emit8(hi + 8 * u, 64 + 8 * u);            // cols 64-127
         l = l * alpha + ls;
         m = m_new;
         sm100::fence_proxy_async_smem();
