@@ -48,6 +48,7 @@ struct AttnArgs {
   int h = 0, B = 0, W = 0, C = 0;
   void* out = nullptr;        // [h][B][W][C]
   int dtype = 0;
+  float* ws = nullptr; size_t ws_elems = 0;   // split-KV fp32 workspace (optional)
 };
 void launch_attn_simt(const AttnArgs& a, cudaStream_t s);
 

@@ -11,6 +11,7 @@
 //   warps 2-5   softmax: thread = query row; S row held in registers (one TMEM read), online
 //               max/sum in fp32 with lazy rescale of the TMEM accumulator; P_j -> bf16 smem.
 #include <cuda.h>
+#include <cstdlib>
 #include "../common.cuh"
 #include "../kernels.h"
 #include "../sm100.cuh"
@@ -24,6 +25,8 @@ struct TcAttnParams {
   int Wbox, Rbox, nWt, ntiles;
   unsigned box_bytes;
   void* out;
+  int nsplit;                 // split-KV: blockIdx.z = b * nsplit + split; partials -> ws
+  float* ws;                  // [nsplit][B][heads][h*W][64 + 2] (O unnormalised, m, l)
 };
 
 namespace {
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int head = blockIdx.y, b = blockIdx.z;
+  const int head = blockIdx.y, b = blockIdx.z / p.nsplit, sp = blockIdx.z % p.nsplit;
   const int nqt = ((p.h + p.Rbox - 1) / p.Rbox) * p.nWt;
   const int qt0 = 2 * blockIdx.x;
   const int nwg = (qt0 + 1 < nqt) ? 2 : 1;          // query tiles in this CTA
@@ -103,7 +106,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
   __syncthreads();
   sm100::fence_after();
   const uint32_t tmem = *tmem_slot;     // cols: S wg0 [0,128), S wg1 [128,256), O wg0 [256,320), O wg1 [320,384)
-  const int nt = p.ntiles;
+  const int j0 = p.ntiles * sp / p.nsplit, j1 = p.ntiles * (sp + 1) / p.nsplit;   // this CTA's key tiles
+  const int nt = j1 - j0;                                                            // tiles are j0 + jj
 
   if (warp == 0) {
     if (lane == 0) {
@@ -112,11 +116,11 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         const int qt = qt0 + g;
         sm100::tma_load_4d(smem + SM_Q + g * TILE, &p.mq, q_full, head * 64, (qt % p.nWt) * p.Wbox, b, (qt / p.nWt) * p.Rbox);
       }
-      for (int j = 0; j < nt; ++j) {
-        const int st = j % KST;
-        sm100::mbar_wait(&kv_empty[st], ((j / KST) & 1) ^ 1);
+      for (int jj = 0; jj < nt; ++jj) {
+        const int st = jj % KST;
+        sm100::mbar_wait(&kv_empty[st], ((jj / KST) & 1) ^ 1);
         int s, r0, w0;
-        tile_coords(p, j, s, r0, w0);
+        tile_coords(p, j0 + jj, s, r0, w0);
         sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * p.box_bytes);
         sm100::tma_load_4d(smem + SM_K + st * TILE, &p.mkv[s], &kv_full[st], head * 64, w0, b, r0);
         sm100::tma_load_4d(smem + SM_V + st * TILE, &p.mkv[s], &kv_full[st], p.C + head * 64, w0, b, r0);
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
       sm100::mbar_wait(q_full, 0);
       auto issue_s = [&](int g, int j) {
         const uint32_t q_base = sm100::smem_u32(smem + SM_Q + g * TILE);
-        const uint32_t k_base = sm100::smem_u32(smem + SM_K + (j % KST) * TILE);
+        const uint32_t k_base = sm100::smem_u32(smem + SM_K + (j % KST) * TILE);   // j: local tile index
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           sm100::mma_bf16_ss(tmem + g * 128, sm100::sdesc_sw128(q_base + k * 32, 16, 1024),
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
       uint8_t* P = smem + SM_P + g * 2 * TILE;
       for (int j = 0; j < nt; ++j) {
         int s, r0, w0;
-        tile_coords(p, j, s, r0, w0);
+        tile_coords(p, j0 + j, s, r0, w0);
         const int nvr = min(p.Rbox, p.rows[s] - r0);
         const int nvw = min(p.Wbox, p.W - w0);
         const int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;   // valid keys form a prefix
@@ -270,7 +274,17 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
       sm100::tmem_wait_ld();
       const int qt = qt0 + g;
       const int r = (qt / p.nWt) * p.Rbox + row / p.Wbox, w = (qt % p.nWt) * p.Wbox + row % p.Wbox;
-      if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
+      if (p.nsplit > 1) {
+        if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
+          const long long tok = (long long)r * p.W + w;
+          float* wp = p.ws + ((((long long)sp * p.B + b) * (p.C / 64) + head) * ((long long)p.h * p.W) + tok) * 66;
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            *reinterpret_cast<float2*>(wp + 4 * u) = make_float2(acc[4 * u], acc[4 * u + 1]),
+            *reinterpret_cast<float2*>(wp + 4 * u + 2) = make_float2(acc[4 * u + 2], acc[4 * u + 3]);
+          *reinterpret_cast<float2*>(wp + 64) = make_float2(m, l);
+        }
+      } else if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
         const float inv = 1.f / l;
 #pragma unroll
         for (int i = 0; i < 64; ++i) acc[i] *= inv;
@@ -300,6 +314,34 @@ static bool encode_tok(CUtensorMap* m, const void* base, int rows, int B, int W,
   return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// split-KV combine: O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s, M = max_s m_s (fixed order)
+__global__ void attn_combine_kernel(const float* __restrict__ ws, int nsplit, int B, int heads, int h, int W,
+                                    int C, bf16* __restrict__ out) {
+  const long long ntok = (long long)h * W;
+  const long long total = (long long)B * heads * ntok;
+  for (long long i = (long long)blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8; i < total;
+       i += (long long)gridDim.x * (blockDim.x / 8)) {
+    const int part = threadIdx.x & 7;                 // 8 threads per row, 8 dims each
+    const long long tok = i % ntok;
+    const int head = (int)((i / ntok) % heads), b = (int)(i / (ntok * heads));
+    float M = -INFINITY;
+    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, ws[(((long long)s * B + b) * heads + head) * ntok * 66 + tok * 66 + 64]);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, L = 0.f;
+    for (int s = 0; s < nsplit; ++s) {
+      const float* wp = ws + ((((long long)s * B + b) * heads + head) * ntok + tok) * 66;
+      const float f = exp2f(wp[64] - M);
+      L += f * wp[65];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += f * wp[part * 8 + e];
+    }
+    const float inv = 1.f / L;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= inv;
+    const int r = (int)(tok / W), w = (int)(tok % W);
+    store8(out + (((long long)r * B + b) * W + w) * C + head * 64 + part * 8, acc);
+  }
 }
 
 bool attn_tc_supported(const AttnArgs& a) {
@@ -333,8 +375,32 @@ bool launch_attn_tc(const AttnArgs& a, cudaStream_t s) {
   }
   for (int i = p.nsrc; i < 3; ++i) p.mkv[i] = p.mkv[0];
   const int qtiles = ((a.h + p.Rbox - 1) / p.Rbox) * p.nWt;
-  dim3 grid((qtiles + 1) / 2, a.C / 64, a.B);
+  const long long ctas = (long long)((qtiles + 1) / 2) * (a.C / 64) * a.B;
+  // split the key range when the (q tile pair, head, b) grid under-fills the 148 SMs
+  p.nsplit = 1; p.ws = a.ws;
+  // split-KV (+ combine) is off by default: measured slower than the unsplit kernel at every
+  // 1024^2 shape (per-CTA prologue + combine); PCPP_ATTN_SPLIT=1 enables it for experiments
+  static const int split_env = getenv("PCPP_ATTN_SPLIT") ? atoi(getenv("PCPP_ATTN_SPLIT")) : 0;
+  if (a.ws && split_env) {
+    double best = (double)ctas / (double)(((ctas + 147) / 148) * 148);
+    for (int sp = 2; sp <= 8; ++sp) {
+      if (p.ntiles / sp < 3) break;
+      const long long need = (long long)sp * a.B * (a.C / 64) * a.h * a.W * 66;
+      if ((size_t)need > a.ws_elems) break;
+      const long long c = ctas * sp;
+      const double e = (double)c / (double)(((c + 147) / 148) * 148) - 0.03 * (sp - 1);
+      if (e > best + 0.05) { best = e; p.nsplit = sp; }
+    }
+  }
+  dim3 grid((qtiles + 1) / 2, a.C / 64, a.B * p.nsplit);
   attn_tc_kernel<<<grid, ATTN_THREADS, ATTN_SMEM, s>>>(p);
+  if (p.nsplit > 1) {
+    const long long rows = (long long)a.B * (a.C / 64) * a.h * a.W;
+    long long blocks = (rows + 31) / 32;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    attn_combine_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.ws, p.nsplit, a.B, a.C / 64, a.h, a.W, a.C,
+                                                         reinterpret_cast<bf16*>(a.out));
+  }
   return true;
 }
 

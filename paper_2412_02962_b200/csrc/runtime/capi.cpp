@@ -432,6 +432,14 @@ pcpp_status pcpp_op_attention(const void* q, const void* const* kv, const int* k
   a.q = q; a.h = h; a.B = B; a.W = W; a.C = C; a.out = out; a.dtype = dtype == PCPP_FP32 ? DT_F32 : DT_BF16;
   a.nsrc = nsrc;
   for (int i = 0; i < nsrc; ++i) { a.src[i].kv = kv[i]; a.src[i].rows = kv_rows[i]; }
+  static float* ws = nullptr; static size_t ws_cap = 0;
+  const size_t need = 8ull * B * (C / 64) * h * W * 66;
+  if (a.dtype == DT_BF16 && need > ws_cap) {
+    if (ws) cudaFree(ws);
+    ws = nullptr; ws_cap = 0;
+    if (cudaMalloc(&ws, need * 4) == cudaSuccess) ws_cap = need;
+  }
+  a.ws = ws; a.ws_elems = ws_cap;
   launch_attn_auto(a, impl == PCPP_KERNELS_AUTO, reinterpret_cast<cudaStream_t>(stream));
   CKS(cudaGetLastError());
   return PCPP_OK;

@@ -529,6 +529,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
             if (i < n - 1 && ax.r > 0) a.src[ns++] = AttnSrc{base + ax.off_bot[1 - par], ax.r};
           }
           a.nsrc = ns;
+          a.ws = P.ws; a.ws_elems = P.ws_elems;
           launch_attn_tc_or_simt(P, a, s);
         }
         P.launches_per_step += nr;
