@@ -63,7 +63,11 @@ CASES = [
     ("sdxl", 32, 2, 0.3, 1, 50, "fp32", "pcpp", 2),
     ("sdxl", 32, 8, 0.8, 1, 50, "bf16", "pcpp", 2),
     ("sdxl", 32, 1, 0.0, 0, 50, "bf16", "pcpp", 2),
+    ("sdxl", 32, 4, 0.8, 1, 50, "bf16", "fullmap", 2),            # X2 analogue: DistriFusion-style
 ]
+
+# config SW analogue: conditioning-fraction sweep at n = 8 (SDXL-shaped, 32x32 latent)
+SWEEP = [("sdxl", 32, 8, p, 1, 50, "bf16", "pcpp", 2) for p in (0.0, 0.125, 0.25, 0.5, 1.0)]
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c)))
@@ -74,6 +78,19 @@ def test_path_matches_oracle(cuda_ok, case):
     errs = [rel_l2(g, r) for g, r in zip(got, ref)]
     print(case, "rel-L2 per step:", ["%.2e" % e for e in errs], "tc:", info["tc_kernels"])
     assert all(e <= TOL[precision] for e in errs), errs
+
+
+@pytest.mark.parametrize("case", SWEEP, ids=lambda c: f"p{c[3]}")
+def test_sweep_cond_fraction_matches_oracle_and_ledger(cuda_ok, case):
+    from oracle import ledger
+    model, H, n, p, w, S, precision, scheme, ms = case
+    ref = oracle_run(*case)
+    got, info = lib_run(*case)
+    errs = [rel_l2(g, r) for g, r in zip(got, ref)]
+    print(case, "rel-L2 per step:", ["%.2e" % e for e in errs])
+    assert all(e <= TOL[precision] for e in errs), errs
+    want = ledger.physical_bytes(model, H, H, n, p, 2, "pcpp_async")
+    assert info["bytes_counted_async"] == [want[c] for c in ("attn", "conv", "gn")]
 
 
 def test_bf16_simt_and_tc_agree_with_oracle(cuda_ok):
