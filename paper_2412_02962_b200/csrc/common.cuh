@@ -9,6 +9,27 @@ typedef __nv_bfloat16 bf16;
 
 namespace pcpp {
 
+// Programmatic dependent launch (PDL): every step kernel triggers its dependents at entry and waits
+// for its predecessor's completion (griddepcontrol.wait) before touching dependent global memory,
+// so a kernel's launch and prologue overlap the previous kernel's tail inside the step graph.
+// Triggering at CTA entry is deadlock-free: dependents launch only once every CTA of this grid
+// has started.  Without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 enum DType : int { DT_F32 = 0, DT_BF16 = 1 };
 
 static inline size_t dtype_size(int dt) { return dt == DT_F32 ? 4 : 2; }

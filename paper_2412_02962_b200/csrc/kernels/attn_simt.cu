@@ -13,6 +13,8 @@ constexpr int QB = 64, KC = 32, HD = 64;
 
 template <typename T>
 __global__ void __launch_bounds__(256) attn_simt_kernel(const AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float Qs[QB][HD];
   __shared__ float Ks[KC][HD + 1];
   __shared__ float Vs[KC][HD];
@@ -104,8 +106,8 @@ __global__ void __launch_bounds__(256) attn_simt_kernel(const AttnArgs a) {
 
 void launch_attn_simt(const AttnArgs& a, cudaStream_t s) {
   dim3 grid((a.h * a.W + QB - 1) / QB, a.C / HD, a.B);
-  if (a.dtype == DT_F32) attn_simt_kernel<float><<<grid, 256, 0, s>>>(a);
-  else attn_simt_kernel<bf16><<<grid, 256, 0, s>>>(a);
+  if (a.dtype == DT_F32) launch_pdl(attn_simt_kernel<float>, dim3(grid), dim3(256), 0, s, a);
+  else launch_pdl(attn_simt_kernel<bf16>, dim3(grid), dim3(256), 0, s, a);
 }
 
 }  // namespace pcpp

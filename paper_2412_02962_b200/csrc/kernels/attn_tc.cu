@@ -66,6 +66,7 @@ __device__ __forceinline__ void tile_coords(const TcAttnParams& p, int j, int& s
 // warpgroup's S / O while the other warpgroup runs its softmax (ping-pong), and each scheduler has
 // two softmax warps to interleave.
 __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_constant__ TcAttnParams p) {
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM_BAR);
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
   sm100::fence_before();
   __syncthreads();
   sm100::fence_after();
+  pdl_wait();                           // Q / K / V are produced by the previous kernels
   const uint32_t tmem = *tmem_slot;     // cols: S wg0 [0,128), S wg1 [128,256), O wg0 [256,320), O wg1 [320,384)
   const int j0 = p.ntiles * sp / p.nsplit, j1 = p.ntiles * (sp + 1) / p.nsplit;   // this CTA's key tiles
   const int nt = j1 - j0;                                                            // tiles are j0 + jj
@@ -319,6 +321,8 @@ static bool encode_tok(CUtensorMap* m, const void* base, int rows, int B, int W,
 // split-KV combine: O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s, M = max_s m_s (fixed order)
 __global__ void attn_combine_kernel(const float* __restrict__ ws, int nsplit, int B, int heads, int h, int W,
                                     int C, bf16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const long long ntok = (long long)h * W;
   const long long total = (long long)B * heads * ntok;
   for (long long i = (long long)blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8; i < total;
@@ -393,12 +397,12 @@ bool launch_attn_tc(const AttnArgs& a, cudaStream_t s) {
     }
   }
   dim3 grid((qtiles + 1) / 2, a.C / 64, a.B * p.nsplit);
-  attn_tc_kernel<<<grid, ATTN_THREADS, ATTN_SMEM, s>>>(p);
+  launch_pdl(attn_tc_kernel, dim3(grid), dim3(ATTN_THREADS), ATTN_SMEM, s, p);
   if (p.nsplit > 1) {
     const long long rows = (long long)a.B * (a.C / 64) * a.h * a.W;
     long long blocks = (rows + 31) / 32;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    attn_combine_kernel<<<(unsigned)blocks, 256, 0, s>>>(p.ws, p.nsplit, a.B, a.C / 64, a.h, a.W, a.C,
+    launch_pdl(attn_combine_kernel, dim3((unsigned)blocks), dim3(256), 0, s, p.ws, p.nsplit, a.B, a.C / 64, a.h, a.W, a.C,
                                                          reinterpret_cast<bf16*>(a.out));
   }
   return true;

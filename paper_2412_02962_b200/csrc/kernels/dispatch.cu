@@ -1,10 +1,16 @@
 // Kernel selection: tcgen05 (sm_100a tensor cores) for the bf16 contractions the TC kernels
 // support, SIMT otherwise (fp32 parity mode, conv_in, odd shapes).
+#include <cstdlib>
 #include "../common.cuh"
 #include "../kernels.h"
 #include "../runtime/runtime.h"
 
 namespace pcpp {
+
+bool pdl_enabled() {
+  static const int on = getenv("PCPP_PDL") ? atoi(getenv("PCPP_PDL")) : 1;
+  return on != 0;
+}
 
 bool tc_available();
 bool gemm_tc_supported(const GemmArgs& g);

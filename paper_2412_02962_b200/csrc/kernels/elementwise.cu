@@ -8,6 +8,8 @@ namespace pcpp {
 
 // ---- latent [h][W][4] fp32 -> xin [h][2][W][4] fp32 (rows 0..h-1; halos untouched) ------------
 __global__ void prep_latent_kernel(const float4* __restrict__ lat, float4* __restrict__ xin, int h, int W) {
+  pdl_trigger();
+  pdl_wait();
   const long long n = (long long)h * W;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / W, w = i % W;
@@ -19,13 +21,15 @@ __global__ void prep_latent_kernel(const float4* __restrict__ lat, float4* __res
 void launch_prep_latent(const float* latent, const ActView& xin, cudaStream_t s) {
   const long long n = (long long)xin.rows * xin.W;
   int blocks = (int)((n + 255) / 256); if (blocks > 1184) blocks = 1184;
-  prep_latent_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(latent),
+  launch_pdl(prep_latent_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const float4*>(latent),
                                              reinterpret_cast<float4*>(xin.base), xin.rows, xin.W);
 }
 
 // ---- nearest x2 upsample (16-byte vectors) ------------------------------------------------------
 __global__ void upsample2_kernel(const uint4* __restrict__ in, uint4* __restrict__ out,
                                  int h, int B, int W, int nv /*16B vectors per token*/) {
+  pdl_trigger();
+  pdl_wait();
   const long long n = (long long)2 * h * B * 2 * W * nv;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int v = (int)(i % nv); long long t = i / nv;
@@ -38,7 +42,7 @@ void launch_upsample2(const ActView& in, const ActView& out, cudaStream_t s) {
   const int nv = (int)(in.C * dtype_size(in.dtype) / 16);
   const long long n = (long long)out.rows * out.B * out.W * nv;
   int blocks = (int)((n + 255) / 256); if (blocks > 1184 * 2) blocks = 1184 * 2;
-  upsample2_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(in.base), reinterpret_cast<uint4*>(out.base),
+  launch_pdl(upsample2_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const uint4*>(in.base), reinterpret_cast<uint4*>(out.base),
                                           in.rows, in.B, in.W, nv);
 }
 
@@ -47,6 +51,8 @@ void launch_upsample2(const ActView& in, const ActView& out, cudaStream_t s) {
 // x' = sqrt(ab_prev) x0 + sqrt(1-ab_prev) eps_hat     (b = 0 uncond, b = 1 cond; reading D11)
 __global__ void cfg_ddim_kernel(const float4* __restrict__ eps, float4* __restrict__ lat, int h, int W,
                                 float s_cfg, const double* __restrict__ coef, const int* __restrict__ k_dev) {
+  pdl_trigger();
+  pdl_wait();
   const int k = *k_dev;
   const float sa = (float)coef[4 * k + 0], s1a = (float)coef[4 * k + 1];
   const float sp = (float)coef[4 * k + 2], s1p = (float)coef[4 * k + 3];
@@ -72,18 +78,22 @@ void launch_cfg_ddim(const float* eps, float* latent, int h, int W, float s_cfg,
                      const int* k_dev, cudaStream_t s) {
   const long long n = (long long)h * W;
   int blocks = (int)((n + 255) / 256); if (blocks > 1184) blocks = 1184;
-  cfg_ddim_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(eps), reinterpret_cast<float4*>(latent),
+  launch_pdl(cfg_ddim_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const float4*>(eps), reinterpret_cast<float4*>(latent),
                                          h, W, s_cfg, coef, k_dev);
 }
 
-__global__ void step_end_kernel(int* k_dev) { *k_dev += 1; }
-void launch_step_end(int* k_dev, cudaStream_t s) { step_end_kernel<<<1, 1, 0, s>>>(k_dev); }
+__global__ void step_end_kernel(int* k_dev) {
+  pdl_trigger();
+  pdl_wait(); *k_dev += 1; }
+void launch_step_end(int* k_dev, cudaStream_t s) { launch_pdl(step_end_kernel, dim3(1), dim3(1), 0, s, k_dev); }
 
 // ---- timestep embedding (reading D19) --------------------------------------------------------
 // hid[j] = SiLU(W1[j] . sinusoid(tau) + b1[j]) ; emb[b][j] = W2[j] . hid + b2[j] (+ cond[j] if b = 1)
 __global__ void temb_hidden_kernel(const float* __restrict__ w1, const float* __restrict__ b1,
                                    const int* __restrict__ taus, const int* __restrict__ k_dev,
                                    int T, int S, float* __restrict__ hid) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float e[];
   const float tau = (float)taus[*k_dev];
   const int half = S / 2;
@@ -105,6 +115,8 @@ __global__ void temb_hidden_kernel(const float* __restrict__ w1, const float* __
 __global__ void temb_out_kernel(const float* __restrict__ w2, const float* __restrict__ b2,
                                 const float* __restrict__ cond, const float* __restrict__ hid, int T,
                                 float* __restrict__ emb) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (row >= T) return;
@@ -119,12 +131,14 @@ __global__ void temb_out_kernel(const float* __restrict__ w2, const float* __res
 }
 void launch_temb(const float* w1, const float* b1, const float* w2, const float* b2, const float* cond,
                  const int* taus, const int* k_dev, int T, int S, float* hid, float* emb, cudaStream_t s) {
-  temb_hidden_kernel<<<(T + 7) / 8, 256, S * sizeof(float), s>>>(w1, b1, taus, k_dev, T, S, hid);
-  temb_out_kernel<<<(T + 7) / 8, 256, 0, s>>>(w2, b2, cond, hid, T, emb);
+  launch_pdl(temb_hidden_kernel, dim3((T + 7) / 8), dim3(256), S * sizeof(float), s, w1, b1, taus, k_dev, T, S, hid);
+  launch_pdl(temb_out_kernel, dim3((T + 7) / 8), dim3(256), 0, s, w2, b2, cond, hid, T, emb);
 }
 // out[b][j] = Wt[j] . SiLU(emb[b]) + bt[j]   for every ResBlock's temb projection at once
 __global__ void temb_proj_kernel(const float* __restrict__ wt, const float* __restrict__ bt,
                                  const float* __restrict__ emb, int T, int J, float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float se[];
   for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) { const float y = emb[i]; se[i] = y / (1.f + expf(-y)); }
   __syncthreads();
@@ -137,13 +151,15 @@ __global__ void temb_proj_kernel(const float* __restrict__ wt, const float* __re
   if (lane == 0) { out[row] = a0 + bt[row]; out[J + row] = a1 + bt[row]; }
 }
 void launch_temb_proj(const float* wt, const float* bt, const float* emb, int T, int J, float* out, cudaStream_t s) {
-  temb_proj_kernel<<<(J + 7) / 8, 256, 2 * T * sizeof(float), s>>>(wt, bt, emb, T, J, out);
+  launch_pdl(temb_proj_kernel, dim3((J + 7) / 8), dim3(256), 2 * T * sizeof(float), s, wt, bt, emb, T, J, out);
 }
 
 // ---- segment copier: pack / unpack / loopback exchange ------------------------------------------
 // One CTA per segment slice; 16-byte vectors, coalesced.  Segments are 16-byte aligned (rows of
 // B*W*C elements with W*C a multiple of 8).
 __global__ void copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg) {
+  pdl_trigger();
+  pdl_wait();
   for (int sidx = blockIdx.y; sidx < nseg; sidx += gridDim.y) {
     const CopySeg sg = segs[sidx];
     const long long nv = (long long)(sg.bytes / 16);
@@ -159,7 +175,7 @@ void launch_copy_segments(const CopySeg* segs_dev, int nseg, unsigned long long 
   if (gx < 1) gx = 1;
   if (gx > 296) gx = 296;
   dim3 grid((unsigned)gx, nseg < 65535 ? nseg : 65535);
-  copy_segments_kernel<<<grid, 256, 0, s>>>(segs_dev, nseg);
+  launch_pdl(copy_segments_kernel, dim3(grid), dim3(256), 0, s, segs_dev, nseg);
 }
 
 void launch_memset_zero(void* p, size_t bytes, cudaStream_t s) { cudaMemsetAsync(p, 0, bytes, s); }

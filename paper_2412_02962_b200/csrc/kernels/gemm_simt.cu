@@ -37,6 +37,8 @@ __device__ __forceinline__ float load_res(const ActView& v, long long idx) {
 
 template <typename TA, typename TW>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const GemmArgs g) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
@@ -120,10 +122,10 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
   const int M = g.rows_out * g.B * g.w_out;
   dim3 grid((M + BM - 1) / BM, (g.N + BN - 1) / BN);
   const int ta = g.a0.dtype;
-  if (ta == DT_F32 && g.wdtype == DT_F32) gemm_simt_kernel<float, float><<<grid, 256, 0, s>>>(g);
-  else if (ta == DT_BF16 && g.wdtype == DT_BF16) gemm_simt_kernel<bf16, bf16><<<grid, 256, 0, s>>>(g);
-  else if (ta == DT_F32 && g.wdtype == DT_BF16) gemm_simt_kernel<float, bf16><<<grid, 256, 0, s>>>(g);
-  else gemm_simt_kernel<bf16, float><<<grid, 256, 0, s>>>(g);
+  if (ta == DT_F32 && g.wdtype == DT_F32) launch_pdl(gemm_simt_kernel<float, float>, dim3(grid), dim3(256), 0, s, g);
+  else if (ta == DT_BF16 && g.wdtype == DT_BF16) launch_pdl(gemm_simt_kernel<bf16, bf16>, dim3(grid), dim3(256), 0, s, g);
+  else if (ta == DT_F32 && g.wdtype == DT_BF16) launch_pdl(gemm_simt_kernel<float, bf16>, dim3(grid), dim3(256), 0, s, g);
+  else launch_pdl(gemm_simt_kernel<bf16, float>, dim3(grid), dim3(256), 0, s, g);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -132,6 +134,8 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
 template <typename TA>
 __global__ void __launch_bounds__(256) conv_out_kernel(const ActView in, const float* __restrict__ w,
                                                         const float* __restrict__ bias, const ActView out) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const long long tok = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   const long long M = (long long)out.rows * out.B * out.W;
@@ -164,8 +168,8 @@ __global__ void __launch_bounds__(256) conv_out_kernel(const ActView in, const f
 void launch_conv_out(const ActView& in, const float* w, const float* bias, const ActView& out, cudaStream_t s) {
   const long long M = (long long)out.rows * out.B * out.W;
   dim3 grid((unsigned)((M + 7) / 8));
-  if (in.dtype == DT_F32) conv_out_kernel<float><<<grid, 256, 0, s>>>(in, w, bias, out);
-  else conv_out_kernel<bf16><<<grid, 256, 0, s>>>(in, w, bias, out);
+  if (in.dtype == DT_F32) launch_pdl(conv_out_kernel<float>, dim3(grid), dim3(256), 0, s, in, w, bias, out);
+  else launch_pdl(conv_out_kernel<bf16>, dim3(grid), dim3(256), 0, s, in, w, bias, out);
 }
 
 }  // namespace pcpp

@@ -44,6 +44,7 @@ struct TcCfg {
 
 template <int BN>
 __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__ TcGemmParams p) {
+  pdl_trigger();
   // Persistent: CTA c handles work units c, c + gridDim.x, ...; a unit = (m tile, n tile, k split).
   // The smem ring (full/empty) runs continuously across units; two TMEM accumulators (tfull/tempty)
   // let the epilogue of unit i overlap the main loop of unit i+1.
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   __syncthreads();
   sm100::fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();                                   // inputs of this GEMM are produced by the previous kernel
 
   const int n_tiles = p.N / BN;
   const int units = p.m_tiles * n_tiles * p.splits;
@@ -291,13 +293,15 @@ bool gemm_tc_supported(const GemmArgs& g) {
 template <int BN>
 static void launch_bn(const TcGemmParams& p, cudaStream_t s) {
   const int units = p.m_tiles * (p.N / BN) * p.splits;
-  gemm_tc_kernel<BN><<<units < 148 ? units : 148, 192, TcCfg<BN>::SMEM, s>>>(p);
+  launch_pdl(gemm_tc_kernel<BN>, dim3(units < 148 ? units : 148), dim3(192), TcCfg<BN>::SMEM, s, p);
 }
 
 // split-K epilogue: out[T][n] = sum_z ws[z][T][n] (fixed order) + bias + temb + residual
 __global__ void gemm_splitk_finish(const float* __restrict__ ws, int splits, long long M, int N, int W, int B,
                                    const float* __restrict__ bias, const float* __restrict__ temb, int temb_ld,
                                    ActView res, ActView out, ActView out2, int n_split) {
+  pdl_trigger();
+  pdl_wait();
   const int nv = N / 8;
   const long long total = M * nv;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -389,7 +393,7 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const long long total = M * (g.N / 8);
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    gemm_splitk_finish<<<(unsigned)blocks, 256, 0, s>>>(p.ws, p.splits, M, g.N, g.w_out, g.B, g.bias, g.temb,
+    launch_pdl(gemm_splitk_finish, dim3((unsigned)blocks), dim3(256), 0, s, p.ws, p.splits, M, g.N, g.w_out, g.B, g.bias, g.temb,
                                                        g.temb_ld, g.res, g.out, g.out2, p.n_split);
   }
   return true;

@@ -142,6 +142,8 @@ __device__ __forceinline__ bool gn_stats_phase(const GnStatsArgs& a, float* red,
 
 template <typename T>
 __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float red[];                   // [ntl][nv][2 b][8][2]
   __shared__ bool amlast;
   gn_stats_phase<T>(a, red, amlast);
@@ -151,8 +153,8 @@ __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
 void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
   const Lanes L = lanes_for(a.C);
   const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
-  if (a.x0.dtype == DT_F32) gn_stats_kernel<float><<<a.nchunk, NT, smem, s>>>(a);
-  else gn_stats_kernel<bf16><<<a.nchunk, NT, smem, s>>>(a);
+  if (a.x0.dtype == DT_F32) launch_pdl(gn_stats_kernel<float>, dim3(a.nchunk), dim3(NT), smem, s, a);
+  else launch_pdl(gn_stats_kernel<bf16>, dim3(a.nchunk), dim3(NT), smem, s, a);
 }
 
 // ---- apply -------------------------------------------------------------------------------------
@@ -247,6 +249,8 @@ __device__ __forceinline__ void gn_apply_phase(const GnApplyArgs& a, const float
 
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int tok_per_cta) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float mu_s[2 * G], rs_s[2 * G];
   gn_prep(a, mu_s, rs_s);
   __syncthreads();
@@ -262,6 +266,8 @@ __global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int t
 // <= 148).  Phase 2 re-reads this CTA's own token range (L2-resident).
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(NT) gn_fused_kernel(const GnStatsArgs sa, const GnApplyArgs aa) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float red[];
   __shared__ bool amlast;
   __shared__ float mu_s[2 * G], rs_s[2 * G];
@@ -296,8 +302,8 @@ void launch_gn_fused(const GnStatsArgs& sa, const GnApplyArgs& aa, cudaStream_t 
   if (a2.nchunk > 148) a2.nchunk = 148;
   const Lanes L = lanes_for(a2.C);
   const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
-  if (a2.x0.dtype == DT_F32) gn_fused_kernel<float, float><<<a2.nchunk, NT, smem, s>>>(a2, aa);
-  else gn_fused_kernel<bf16, bf16><<<a2.nchunk, NT, smem, s>>>(a2, aa);
+  if (a2.x0.dtype == DT_F32) launch_pdl(gn_fused_kernel<float, float>, dim3(a2.nchunk), dim3(NT), smem, s, a2, aa);
+  else launch_pdl(gn_fused_kernel<bf16, bf16>, dim3(a2.nchunk), dim3(NT), smem, s, a2, aa);
 }
 
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
@@ -306,8 +312,8 @@ void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
   long long per = (long long)L.ntl * 8;                           // ~8 tokens per token lane
   long long blocks = (ntok + per - 1) / per;
   if (blocks > 148 * 8) { blocks = 148 * 8; per = (ntok + blocks - 1) / blocks; }
-  if (a.x0.dtype == DT_F32) gn_apply_kernel<float, float><<<(unsigned)blocks, NT, 0, s>>>(a, (int)per);
-  else gn_apply_kernel<bf16, bf16><<<(unsigned)blocks, NT, 0, s>>>(a, (int)per);
+  if (a.x0.dtype == DT_F32) launch_pdl(gn_apply_kernel<float, float>, dim3((unsigned)blocks), dim3(NT), 0, s, a, (int)per);
+  else launch_pdl(gn_apply_kernel<bf16, bf16>, dim3((unsigned)blocks), dim3(NT), 0, s, a, (int)per);
 }
 
 void gn_init() {   // dynamic smem: ntl * nv * 32 floats <= 40 KB (C <= 2560)
