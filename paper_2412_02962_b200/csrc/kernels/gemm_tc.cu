@@ -13,6 +13,8 @@
 #include <cuda.h>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include "../common.cuh"
 #include "../kernels.h"
 #include "../sm100.cuh"
@@ -345,10 +347,33 @@ void gemm_tc_init() {
   cudaFuncSetAttribute(gemm_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<64>::SMEM);
 }
 
-bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
+// ---- configuration choice: per-shape autotune cache (filled at plan time), else a heuristic ----
+struct GemmKey {
+  int rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt;
+  bool operator<(const GemmKey& o) const {
+    const int a[11] = {rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt};
+    const int b[11] = {o.rows_out, o.w_out, o.B, o.N, o.cin, o.c0, o.taps, o.stride, o.split_out, o.res, o.odt};
+    for (int i = 0; i < 11; ++i) if (a[i] != b[i]) return a[i] < b[i];
+    return false;
+  }
+};
+static GemmKey key_of(const GemmArgs& g) {
+  return GemmKey{g.rows_out, g.w_out, g.B, g.N, g.cin, g.c0, g.taps, g.stride, g.n_split < g.N ? g.n_split : 0,
+                 g.res.base ? 1 : 0, g.out.dtype};
+}
+struct GemmChoice { int bn, splits; };
+static std::map<GemmKey, GemmChoice>& tune_cache() { static std::map<GemmKey, GemmChoice> m; return m; }
+static std::mutex& tune_mu() { static std::mutex m; return m; }
+
+static bool bn_ok(const GemmArgs& g, int bn) {
+  if (g.N % bn) return false;
+  if (g.n_split < g.N && g.n_split % bn) return false;
+  return true;
+}
+
+static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int want_splits) {
   TcGemmParams p;
   memset(&p, 0, sizeof p);
-  const int BN = pick_bn(g);
   // tile geometry: 128 output tokens = Wbox x Bbox x Rbox in (w, b, r) layout order
   if (g.w_out >= 128) { p.Wbox = 128; p.Bbox = 1; p.Rbox = 1; }
   else if (g.B == 2 && 128 % (2 * g.w_out) == 0) { p.Wbox = g.w_out; p.Bbox = 2; p.Rbox = 128 / (2 * g.w_out); }
@@ -366,21 +391,11 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   if (!encode_act(&p.ma0, g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_act(&p.ma1, g.a1.base ? g.a1 : g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN)) return false;
-  // split-K when the output tiles fill the 148 SMs poorly (small M: level 2, or n > 1 patches)
   const int nsteps = p.taps * p.nkc;
-  const long long tiles = (long long)p.m_tiles * (g.N / BN);
   const long long M = (long long)g.rows_out * g.B * g.w_out;
   p.splits = 1; p.s_len = nsteps; p.ws = g.ws;
-  static const int splitk_env = getenv("PCPP_SPLITK") ? atoi(getenv("PCPP_SPLITK")) : 1;
-  if (splitk_env && g.ws && tiles < 148) {
-    double best = wave_eff(tiles);
-    for (int S = 2; S <= 8; ++S) {
-      if (nsteps / S < 8) break;
-      if ((size_t)S * M * g.N > g.ws_elems) break;
-      const double e = wave_eff(tiles * S) - 0.02 * (S - 1);
-      if (e > best + 0.05) { best = e; p.splits = S; }
-    }
-    p.s_len = (nsteps + p.splits - 1) / p.splits;
+  if (want_splits > 1 && g.ws && (size_t)want_splits * M * g.N <= g.ws_elems) {
+    p.s_len = (nsteps + want_splits - 1) / want_splits;
     p.splits = (nsteps + p.s_len - 1) / p.s_len;
   }
   switch (BN) {
@@ -393,10 +408,76 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
     const long long total = M * (g.N / 8);
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    launch_pdl(gemm_splitk_finish, dim3((unsigned)blocks), dim3(256), 0, s, p.ws, p.splits, M, g.N, g.w_out, g.B, g.bias, g.temb,
-                                                       g.temb_ld, g.res, g.out, g.out2, p.n_split);
+    launch_pdl(gemm_splitk_finish, dim3((unsigned)blocks), dim3(256), 0, s, p.ws, p.splits, M, g.N, g.w_out, g.B,
+               g.bias, g.temb, g.temb_ld, g.res, g.out, g.out2, p.n_split);
   }
   return true;
+}
+
+static GemmChoice heuristic(const GemmArgs& g) {
+  GemmChoice c{pick_bn(g), 1};
+  const int m_tiles = g.w_out >= 128 ? g.rows_out * g.B * ((g.w_out + 127) / 128)
+                      : (g.B == 2 && 128 % (2 * g.w_out) == 0) ? (g.rows_out + 128 / (2 * g.w_out) - 1) / (128 / (2 * g.w_out))
+                      : g.rows_out * g.B;
+  const long long tiles = (long long)m_tiles * (g.N / c.bn);
+  const int nsteps = g.taps * (g.cin / 64);
+  const long long M = (long long)g.rows_out * g.B * g.w_out;
+  static const int splitk_env = getenv("PCPP_SPLITK") ? atoi(getenv("PCPP_SPLITK")) : 1;
+  if (splitk_env && g.ws && tiles < 148) {
+    double best = wave_eff(tiles);
+    for (int S = 2; S <= 8; ++S) {
+      if (nsteps / S < 8) break;
+      if ((size_t)S * M * g.N > g.ws_elems) break;
+      const double e = wave_eff(tiles * S) - 0.02 * (S - 1);
+      if (e > best + 0.05) { best = e; c.splits = S; }
+    }
+  }
+  return c;
+}
+
+bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
+  GemmChoice c;
+  {
+    std::lock_guard<std::mutex> lk(tune_mu());
+    auto it = tune_cache().find(key_of(g));
+    c = it != tune_cache().end() ? it->second : heuristic(g);
+  }
+  return launch_gemm_tc_cfg(g, s, c.bn, c.splits);
+}
+
+// Time every legal (BN, split-K) configuration of this GEMM shape on its real buffers and cache the
+// fastest (called at plan time, outside graph capture; outputs are scratch at that point).
+void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
+  if (!gemm_tc_supported(g)) return;
+  const GemmKey key = key_of(g);
+  {
+    std::lock_guard<std::mutex> lk(tune_mu());
+    if (tune_cache().count(key)) return;
+  }
+  const int nsteps = g.taps * (g.cin / 64);
+  const long long M = (long long)g.rows_out * g.B * g.w_out;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  GemmChoice best = heuristic(g);
+  float best_ms = 1e30f;
+  const int bns[4] = {256, 160, 128, 64};
+  for (int bn : bns) {
+    if (!bn_ok(g, bn)) continue;
+    for (int S = 1; S <= 6; ++S) {
+      if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems)) break;
+      if (!launch_gemm_tc_cfg(g, s, bn, S)) continue;      // warm
+      cudaEventRecord(e0, s);
+      for (int r = 0; r < 3; ++r) launch_gemm_tc_cfg(g, s, bn, S);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best_ms * 0.97f) { best_ms = ms; best = GemmChoice{bn, S}; }
+    }
+  }
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  std::lock_guard<std::mutex> lk(tune_mu());
+  tune_cache()[key] = best;
 }
 
 }  // namespace pcpp

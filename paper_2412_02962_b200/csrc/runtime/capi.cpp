@@ -216,6 +216,7 @@ pcpp_status pcpp_plan(int H, int W, int C, int n, double p, int w, const pcpp_co
   CKS(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   CKS(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   if ((st = plan_init_comm(P)) != PCPP_OK) return st;
+  if ((st = plan_autotune(P)) != PCPP_OK) return st;
   CKS(cudaDeviceSynchronize());
   *out = h.release();
   return PCPP_OK;

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <dlfcn.h>
+#include <cstdlib>
 #include "runtime.h"
 #include "nccl_api.h"
 
@@ -402,6 +403,42 @@ static unsigned op_kind(OpK k) {
     case OP_END: return K_END;
     default: return K_MISC;
   }
+}
+
+void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s);
+bool gemm_tc_supported(const GemmArgs& g);
+
+// Per-shape GEMM configuration search on the plan's own buffers (before any graph capture).
+pcpp_status plan_autotune(Plan& P) {
+  if (!P.use_tc) return PCPP_OK;
+  static const int env = getenv("PCPP_AUTOTUNE") ? atoi(getenv("PCPP_AUTOTUNE")) : 1;
+  if (!env) return PCPP_OK;
+  const size_t es = dtype_size(P.dtype);
+  const char* wm = reinterpret_cast<const char*>(P.wmat);
+  for (const Op& op : P.ops) {
+    if (op.k != OP_CONV && op.k != OP_GEMM) continue;
+    GemmArgs g;
+    g.a0 = view(P, 0, op.in0, 0);
+    g.c0 = g.a0.C; g.cin = g.a0.C;
+    if (op.in1 >= 0) { g.a1 = view(P, 0, op.in1, 0); g.cin += g.a1.C; }
+    g.taps = op.k == OP_CONV ? 9 : 1;
+    g.stride = op.stride;
+    const ActView o = view(P, 0, op.out, 0);
+    g.rows_out = o.rows; g.w_out = o.W; g.B = B_CFG;
+    g.w = op.w_f32 ? (const void*)(P.wf32 + op.w) : (const void*)(wm + (size_t)op.w * es);
+    g.wdtype = op.w_f32 ? DT_F32 : P.dtype;
+    g.N = op.N;
+    g.bias = op.b >= 0 ? P.wf32 + op.b : nullptr;
+    if (op.temb_off >= 0) { g.temb = P.tproj + op.temb_off; g.temb_ld = P.J; }
+    if (op.res >= 0) g.res = view(P, 0, op.res, 0);
+    g.out = o;
+    if (op.out2 >= 0) { g.out2 = view(P, 0, op.out2, 0); g.n_split = op.n_split; }
+    g.ws = P.ws; g.ws_elems = P.ws_elems;
+    if (gemm_tc_supported(g)) gemm_tc_autotune(g, P.s0);
+  }
+  CK(cudaStreamSynchronize(P.s0));
+  CK(cudaGetLastError());
+  return PCPP_OK;
 }
 
 pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {

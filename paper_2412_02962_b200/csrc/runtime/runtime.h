@@ -136,6 +136,7 @@ pcpp_status plan_allocate(Plan& P);
 pcpp_status plan_upload_weights(Plan& P, const float* blob);
 pcpp_status plan_build_exchanges(Plan& P);
 pcpp_status plan_init_comm(Plan& P);
+pcpp_status plan_autotune(Plan& P);
 enum { K_GEMM = 1, K_ATTN = 2, K_GN = 4, K_XCH = 8, K_MISC = 16, K_END = 32, K_ALL = 63 };
 pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask = K_ALL);
 // algorithmic work of the ops of one kind in one step (all virtual ranks): flops, bytes, launches
