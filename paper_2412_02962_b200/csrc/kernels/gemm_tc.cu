@@ -39,7 +39,7 @@ struct TcCfg {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (196608 / STAGE) > 8 ? 8 : (196608 / STAGE);
+  static constexpr int STAGES = (223232 / STAGE) > 10 ? 10 : (223232 / STAGE);   // <= 218 KB of smem
   static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;   // 2 accumulators
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
 };
