@@ -44,6 +44,71 @@ struct TcCfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
 };
 
+// epilogue of one 128 x BN accumulator tile held in TMEM (this thread = one row): bias + temb +
+// residual -> bf16/fp32 store, or raw fp32 partials for split-K
+template <int BN>
+__device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t tacc, int r, int b, int w, bool valid,
+                                              int n0, int z) {
+  const bool second = n0 >= p.n_split;
+  const ActView& ov = second ? p.out2 : p.out;
+  const int ncol0 = second ? n0 - p.n_split : n0;
+  const long long orow = (((long long)r * ov.B + b) * ov.W + w) * ov.C + ncol0;
+  const long long rrow = p.res.base ? (((long long)r * p.res.B + b) * p.res.W + w) * p.res.C + n0 : 0;
+  if (p.splits > 1) {
+    // split-K: raw fp32 partial tile -> workspace; gemm_splitk_finish applies the epilogue
+    const long long T = ((long long)r * p.B + b) * p.w_out + w;
+    float* wp = p.ws + ((long long)z * p.rows_out * p.B * p.w_out + T) * p.N + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t v[32];
+      sm100::tmem_ld32(tacc + c, v);
+      sm100::tmem_wait_ld();
+      if (!valid) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<float4*>(wp + c + 4 * j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                                __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t v[32];
+      sm100::tmem_ld32(tacc + c, v);
+      sm100::tmem_wait_ld();
+      if (!valid) continue;
+      float f[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+      if (p.bias) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n0 + c + i);
+      }
+      if (p.temb) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) f[i] += __ldg(p.temb + b * p.temb_ld + n0 + c + i);
+      }
+      if (p.res.base) {
+        float rv[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          load8(reinterpret_cast<const bf16*>(p.res.base) + rrow + c + 8 * j, rv);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[8 * j + i] += rv[i];
+        }
+      }
+      if (ov.dtype == DT_BF16) {
+        bf16* po = reinterpret_cast<bf16*>(ov.base) + orow + c;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
+      } else {
+        float* po = reinterpret_cast<float*>(ov.base) + orow + c;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
+      }
+    }
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
@@ -154,64 +219,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       sm100::mbar_wait(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
       const uint32_t tacc = tmem + a * BN + (uint32_t(q * 32) << 16);
-      const bool second = n0 >= p.n_split;
-      const ActView& ov = second ? p.out2 : p.out;
-      const int ncol0 = second ? n0 - p.n_split : n0;
-      const long long orow = (((long long)r * ov.B + b) * ov.W + w) * ov.C + ncol0;
-      const long long rrow = p.res.base ? (((long long)r * p.res.B + b) * p.res.W + w) * p.res.C + n0 : 0;
-      if (p.splits > 1) {
-        // split-K: raw fp32 partial tile -> workspace; gemm_splitk_finish applies the epilogue
-        const long long T = ((long long)r * p.B + b) * p.w_out + w;
-        float* wp = p.ws + ((long long)z * p.rows_out * p.B * p.w_out + T) * p.N + n0;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t v[32];
-          sm100::tmem_ld32(tacc + c, v);
-          sm100::tmem_wait_ld();
-          if (!valid) continue;
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(wp + c + 4 * j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                                                    __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-        }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t v[32];
-          sm100::tmem_ld32(tacc + c, v);
-          sm100::tmem_wait_ld();
-          if (!valid) continue;
-          float f[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-          if (p.bias) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n0 + c + i);
-          }
-          if (p.temb) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) f[i] += __ldg(p.temb + b * p.temb_ld + n0 + c + i);
-          }
-          if (p.res.base) {
-            float rv[8];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              load8(reinterpret_cast<const bf16*>(p.res.base) + rrow + c + 8 * j, rv);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) f[8 * j + i] += rv[i];
-            }
-          }
-          if (ov.dtype == DT_BF16) {
-            bf16* po = reinterpret_cast<bf16*>(ov.base) + orow + c;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
-          } else {
-            float* po = reinterpret_cast<float*>(ov.base) + orow + c;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
-          }
-        }
-      }
+      gemm_epilogue<BN>(p, tacc, r, b, w, valid, n0, z);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
@@ -298,6 +306,157 @@ static void launch_bn(const TcGemmParams& p, cudaStream_t s) {
   launch_pdl(gemm_tc_kernel<BN>, dim3(units < 148 ? units : 148), dim3(192), TcCfg<BN>::SMEM, s, p);
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2): a CTA pair computes a 256 x BN tile with one tcgen05.mma stream
+// issued by the leader.  Each CTA stages its own 128 A rows and half of the BN B rows per K step,
+// so per-SM smem traffic per MMA cycle drops by ~30% and the ring gets deeper -- the 1-CTA kernel
+// is TMA-latency bound (profiles/r1_ncu_gemm_*).
+// ---------------------------------------------------------------------------------------------
+template <int BN>
+struct TcCfg2 {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = (BN / 2) * 128;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (223232 / STAGE) > 10 ? 10 : (223232 / STAGE);
+  static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant__ TcGemmParams p) {
+  pdl_trigger();
+  using Cfg = TcCfg2<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;     // [2]
+  uint64_t* tempty = tfull + 2;              // [2] (leader's counts both CTAs' epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_rank();
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&p.ma0); sm100::tma_prefetch(&p.ma1); sm100::tma_prefetch(&p.mb);
+    for (int s = 0; s < Cfg::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 8); }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc2<Cfg::TMEM_COLS>(tmem_slot);
+  sm100::fence_before();
+  sm100::cluster_sync();
+  sm100::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  const int n_tiles = p.N / BN;
+  const int m_pairs = (p.m_tiles + 1) / 2;
+  const int units = m_pairs * n_tiles * p.splits;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nsteps_all = p.taps * p.nkc;
+  auto decode = [&](int u, int& r0, int& b0, int& w0, int& n0, int& z) {
+    const int mp = u % m_pairs;
+    const int rest = u / m_pairs;
+    n0 = (rest % n_tiles) * BN;
+    z = rest / n_tiles;
+    const int mt = 2 * mp + (int)rank;
+    if (p.Bbox == 2) { r0 = mt * p.Rbox; b0 = 0; w0 = 0; }
+    else { const int wt = mt % p.nWt; const int tb = mt / p.nWt; b0 = tb % p.B; r0 = tb / p.B; w0 = wt * p.Wbox; }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int u = cid; u < units; u += ncl) {
+        int r0, b0, w0, n0, z;
+        decode(u, r0, b0, w0, n0, z);
+        const int s_begin = z * p.s_len, s_end = min(nsteps_all, s_begin + p.s_len);
+        for (int s = s_begin; s < s_end; ++s, ++it) {
+          const int st = it % Cfg::STAGES;
+          const uint32_t ph = (it / Cfg::STAGES) & 1;
+          sm100::mbar_wait_cluster(&empty[st], ph ^ 1);
+          const int tap = s / p.nkc, kc = s - tap * p.nkc;
+          const int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
+          if (rank == 0) sm100::mbar_arrive_expect_tx(&full[st], 2 * (p.a_bytes + Cfg::B_BYTES));
+          const uint32_t fb = sm100::leader_addr(&full[st]);
+          if (kc < p.nk0)
+            sm100::tma_load_4d_2sm(sA + st * Cfg::A_BYTES, &p.ma0, fb, kc * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
+          else
+            sm100::tma_load_4d_2sm(sA + st * Cfg::A_BYTES, &p.ma1, fb, (kc - p.nk0) * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
+          sm100::tma_load_2d_2sm(sB + st * Cfg::B_BYTES, &p.mb, fb, s * 64, n0 + (int)rank * (BN / 2));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(256, BN, 0, 0);
+      int it = 0, tc = 0;
+      for (int u = cid; u < units; u += ncl, ++tc) {
+        int r0, b0, w0, n0, z;
+        decode(u, r0, b0, w0, n0, z);
+        const int s_begin = z * p.s_len, s_end = min(nsteps_all, s_begin + p.s_len);
+        const int a = tc & 1;
+        sm100::mbar_wait_cluster(&tempty[a], ((tc >> 1) & 1) ^ 1);
+        sm100::fence_after();
+        const uint32_t d = tmem + a * BN;
+        for (int s = s_begin; s < s_end; ++s, ++it) {
+          const int st = it % Cfg::STAGES;
+          const uint32_t ph = (it / Cfg::STAGES) & 1;
+          sm100::mbar_wait_cluster(&full[st], ph);
+          sm100::fence_after();
+          const uint32_t a_base = sm100::smem_u32(sA + st * Cfg::A_BYTES);
+          const uint32_t b_base = sm100::smem_u32(sB + st * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            sm100::mma2_bf16_ss(d, sm100::sdesc_sw128(a_base + k * 32, 16, 1024), sm100::sdesc_sw128(b_base + k * 32, 16, 1024),
+                                idesc, ((s - s_begin) | k) != 0);
+          sm100::mma2_commit_mc(&empty[st], 0x3);
+        }
+        sm100::mma2_commit_mc(&tfull[a], 0x3);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int m = q * 32 + lane;
+    const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
+    int tc = 0;
+    for (int u = cid; u < units; u += ncl, ++tc) {
+      int r0, b0, w0, n0, z;
+      decode(u, r0, b0, w0, n0, z);
+      const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
+      const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
+      const int a = tc & 1;
+      sm100::mbar_wait_cluster(&tfull[a], (tc >> 1) & 1);
+      sm100::fence_after();
+      gemm_epilogue<BN>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z);
+      sm100::fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
+    }
+  }
+  sm100::fence_before();
+  sm100::cluster_sync();
+  if (warp == 1) sm100::tmem_dealloc2<Cfg::TMEM_COLS>(tmem);
+}
+
+template <int BN>
+static void launch_bn2(const TcGemmParams& p, cudaStream_t s) {
+  const int units = ((p.m_tiles + 1) / 2) * (p.N / BN) * p.splits;
+  const int clusters = units < 74 ? units : 74;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(192); cfg.dynamicSmemBytes = TcCfg2<BN>::SMEM; cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at; cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN>, p);
+}
+
 // split-K epilogue: out[T][n] = sum_z ws[z][T][n] (fixed order) + bias + temb + residual
 __global__ void gemm_splitk_finish(const float* __restrict__ ws, int splits, long long M, int N, int W, int B,
                                    const float* __restrict__ bias, const float* __restrict__ temb, int temb_ld,
@@ -341,6 +500,9 @@ static double wave_eff(long long ctas) {
 }
 
 void gemm_tc_init() {
+  cudaFuncSetAttribute(gemm_tc2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<256>::SMEM);
+  cudaFuncSetAttribute(gemm_tc2_kernel<160>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<160>::SMEM);
+  cudaFuncSetAttribute(gemm_tc2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<128>::SMEM);
   cudaFuncSetAttribute(gemm_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
   cudaFuncSetAttribute(gemm_tc_kernel<160>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<160>::SMEM);
   cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<128>::SMEM);
@@ -361,7 +523,7 @@ static GemmKey key_of(const GemmArgs& g) {
   return GemmKey{g.rows_out, g.w_out, g.B, g.N, g.cin, g.c0, g.taps, g.stride, g.n_split < g.N ? g.n_split : 0,
                  g.res.base ? 1 : 0, g.out.dtype};
 }
-struct GemmChoice { int bn, splits; };
+struct GemmChoice { int bn, splits, pair; };
 static std::map<GemmKey, GemmChoice>& tune_cache() { static std::map<GemmKey, GemmChoice> m; return m; }
 static std::mutex& tune_mu() { static std::mutex m; return m; }
 
@@ -371,7 +533,7 @@ static bool bn_ok(const GemmArgs& g, int bn) {
   return true;
 }
 
-static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int want_splits) {
+static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int want_splits, int pair) {
   TcGemmParams p;
   memset(&p, 0, sizeof p);
   // tile geometry: 128 output tokens = Wbox x Bbox x Rbox in (w, b, r) layout order
@@ -398,11 +560,21 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
     p.s_len = (nsteps + want_splits - 1) / want_splits;
     p.splits = (nsteps + p.s_len - 1) / p.s_len;
   }
-  switch (BN) {
-    case 256: launch_bn<256>(p, s); break;
-    case 160: launch_bn<160>(p, s); break;
-    case 128: launch_bn<128>(p, s); break;
-    default: launch_bn<64>(p, s); break;
+  if (pair) {
+    // B box carries BN/2 rows per CTA
+    if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN / 2)) return false;
+    switch (BN) {
+      case 256: launch_bn2<256>(p, s); break;
+      case 160: launch_bn2<160>(p, s); break;
+      default: launch_bn2<128>(p, s); break;
+    }
+  } else {
+    switch (BN) {
+      case 256: launch_bn<256>(p, s); break;
+      case 160: launch_bn<160>(p, s); break;
+      case 128: launch_bn<128>(p, s); break;
+      default: launch_bn<64>(p, s); break;
+    }
   }
   if (p.splits > 1) {
     const long long total = M * (g.N / 8);
@@ -415,7 +587,7 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
 }
 
 static GemmChoice heuristic(const GemmArgs& g) {
-  GemmChoice c{pick_bn(g), 1};
+  GemmChoice c{pick_bn(g), 1, 0};
   const int m_tiles = g.w_out >= 128 ? g.rows_out * g.B * ((g.w_out + 127) / 128)
                       : (g.B == 2 && 128 % (2 * g.w_out) == 0) ? (g.rows_out + 128 / (2 * g.w_out) - 1) / (128 / (2 * g.w_out))
                       : g.rows_out * g.B;
@@ -436,13 +608,20 @@ static GemmChoice heuristic(const GemmArgs& g) {
 }
 
 bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
+  // PCPP_GEMM_FORCE="bn,splits,pair" pins one configuration (testing the variants)
+  static const char* force = getenv("PCPP_GEMM_FORCE");
+  if (force) {
+    int bn = 0, sp = 1, pr = 0;
+    if (sscanf(force, "%d,%d,%d", &bn, &sp, &pr) >= 1 && bn_ok(g, bn) && !(pr && bn == 64))
+      return launch_gemm_tc_cfg(g, s, bn, sp, pr);
+  }
   GemmChoice c;
   {
     std::lock_guard<std::mutex> lk(tune_mu());
     auto it = tune_cache().find(key_of(g));
     c = it != tune_cache().end() ? it->second : heuristic(g);
   }
-  return launch_gemm_tc_cfg(g, s, c.bn, c.splits);
+  return launch_gemm_tc_cfg(g, s, c.bn, c.splits, c.pair);
 }
 
 // Time every legal (BN, split-K) configuration of this GEMM shape on its real buffers and cache the
@@ -461,18 +640,21 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
   GemmChoice best = heuristic(g);
   float best_ms = 1e30f;
   const int bns[4] = {256, 160, 128, 64};
+  static const int pair_env = getenv("PCPP_PAIR") ? atoi(getenv("PCPP_PAIR")) : 1;
+  for (int pair = 0; pair <= (pair_env ? 1 : 0); ++pair)
   for (int bn : bns) {
     if (!bn_ok(g, bn)) continue;
+    if (pair && bn == 64) continue;
     for (int S = 1; S <= 6; ++S) {
       if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems)) break;
-      if (!launch_gemm_tc_cfg(g, s, bn, S)) continue;      // warm
+      if (!launch_gemm_tc_cfg(g, s, bn, S, pair)) continue;      // warm
       cudaEventRecord(e0, s);
-      for (int r = 0; r < 3; ++r) launch_gemm_tc_cfg(g, s, bn, S);
+      for (int r = 0; r < 3; ++r) launch_gemm_tc_cfg(g, s, bn, S, pair);
       cudaEventRecord(e1, s);
       cudaEventSynchronize(e1);
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e0, e1);
-      if (ms < best_ms * 0.97f) { best_ms = ms; best = GemmChoice{bn, S}; }
+      if (ms < best_ms * 0.97f) { best_ms = ms; best = GemmChoice{bn, S, pair}; }
     }
   }
   cudaEventDestroy(e0); cudaEventDestroy(e1);
