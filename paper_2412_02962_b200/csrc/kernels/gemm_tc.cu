@@ -32,6 +32,7 @@ struct TcGemmParams {
   ActView res, out, out2;
   int splits, s_len;          // split-K: blockIdx.z covers k-steps [z*s_len, (z+1)*s_len)
   float* ws;                  // [splits][M][N] fp32 partials (M = tokens in layout order)
+  int epi_skip;               // experiment only (PCPP_EPI_SKIP): drop the epilogue math/stores
 };
 
 template <int BN>
@@ -75,17 +76,25 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
       uint32_t v[32];
       sm100::tmem_ld32(tacc + c, v);
       sm100::tmem_wait_ld();
-      if (!valid) continue;
+      if (!valid || p.epi_skip) continue;
       float f[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-      if (p.bias) {
+      if (p.bias) {                       // 16-byte vector loads (warp-uniform addresses: L1 broadcast)
+        const float4* bp = reinterpret_cast<const float4*>(p.bias + n0 + c);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] += __ldg(p.bias + n0 + c + i);
+        for (int i = 0; i < 8; ++i) {
+          const float4 t = __ldg(bp + i);
+          f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
+        }
       }
       if (p.temb) {
+        const float4* tp = reinterpret_cast<const float4*>(p.temb + b * p.temb_ld + n0 + c);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] += __ldg(p.temb + b * p.temb_ld + n0 + c + i);
+        for (int i = 0; i < 8; ++i) {
+          const float4 t = __ldg(tp + i);
+          f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
+        }
       }
       if (p.res.base) {
         float rv[8];
@@ -550,6 +559,8 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   p.a_bytes = 128u * p.Wbox * p.Bbox * p.Rbox;
   p.bias = g.bias; p.temb = g.temb; p.temb_ld = g.temb_ld;
   p.res = g.res; p.out = g.out; p.out2 = g.out2;
+  static const int epi_skip = getenv("PCPP_EPI_SKIP") ? atoi(getenv("PCPP_EPI_SKIP")) : 0;
+  p.epi_skip = epi_skip;
   if (!encode_act(&p.ma0, g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_act(&p.ma1, g.a1.base ? g.a1 : g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN)) return false;
