@@ -32,6 +32,10 @@ struct GemmArgs {
   ActView res;                               // residual with out's geometry (base==nullptr: none)
   ActView out, out2; int n_split = 1 << 30;  // cols >= n_split -> out2[col - n_split]
   float* ws = nullptr; size_t ws_elems = 0;  // split-K fp32 workspace (optional)
+  // optional fused GroupNorm(32) statistics of `out` (tcgen05 path only): partial sums land in
+  // gn_part [slots][B=2][G=32][2] fp32 and *gn_slots (host) receives the slot count, 0 if the
+  // launch did not produce them (the consumer then runs the standalone stats kernel)
+  float* gn_part = nullptr; int* gn_slots = nullptr;
 };
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 
@@ -61,6 +65,9 @@ struct GnStatsArgs {
   int nchunk = 0;
 };
 void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s);
+// m_out[b][g][k] = sum over slots of part[slot][b][g][k] (fp64, fixed order): the finalize of the
+// GEMM-epilogue-fused statistics
+void launch_gn_finalize(const float* part, int nslots, double* m_out, cudaStream_t s);
 int gn_stats_chunks(int rows, int W);
 void gn_init();
 

@@ -18,6 +18,7 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
 void gemm_tc_init();
 
 void launch_gemm_auto(const GemmArgs& g, bool allow_tc, cudaStream_t s) {
+  if (g.gn_slots) *g.gn_slots = 0;
   if (allow_tc && gemm_tc_supported(g) && launch_gemm_tc(g, s)) return;
   launch_gemm_simt(g, s);
 }

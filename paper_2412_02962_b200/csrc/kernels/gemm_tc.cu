@@ -33,23 +33,108 @@ struct TcGemmParams {
   int splits, s_len;          // split-K: blockIdx.z covers k-steps [z*s_len, (z+1)*s_len)
   float* ws;                  // [splits][M][N] fp32 partials (M = tokens in layout order)
   int epi_skip;               // experiment only (PCPP_EPI_SKIP): drop the epilogue math/stores
+  float* gn_part;             // fused GroupNorm statistics: [gridDim.x * 4 warps][B=2][G=32][2] fp32
+  int gn_cg;                  //   channels per group (N / 32)
 };
 
-template <int BN>
+// Extra shared memory of the stats-fused variant: per epilogue warp a 32 x 17-word bf16 transpose
+// tile (conflict-free row writes / column reads) and the warp's [2][32][2] fp32 group accumulators.
+constexpr int ST_TILE_WORDS = 32 * 17;
+constexpr int ST_SMEM = 4 * ST_TILE_WORDS * 4 + 4 * 128 * 4;
+
+template <int BN, bool ST = false>
 struct TcCfg {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (223232 / STAGE) > 10 ? 10 : (223232 / STAGE);   // <= 218 KB of smem
+  static constexpr int RING = 223232 - (ST ? ST_SMEM : 0);                      // <= 218 KB of smem in all
+  static constexpr int STAGES = (RING / STAGE) > 10 ? 10 : (RING / STAGE);
   static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;   // 2 accumulators
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + (ST ? ST_SMEM : 0);
 };
 
 // epilogue of one 128 x BN accumulator tile held in TMEM (this thread = one row): bias + temb +
 // residual -> bf16/fp32 store, or raw fp32 partials for split-K
-template <int BN>
+// bias + temb + residual for one row's 32-column chunk starting at column n0 + c
+__device__ __forceinline__ void epilogue_math(const TcGemmParams& p, float* f, int b, long long rrow, int n0, int c) {
+  if (p.bias) {                       // 16-byte vector loads (warp-uniform addresses: L1 broadcast)
+    const float4* bp = reinterpret_cast<const float4*>(p.bias + n0 + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 t = __ldg(bp + i);
+      f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
+    }
+  }
+  if (p.temb) {
+    const float4* tp = reinterpret_cast<const float4*>(p.temb + b * p.temb_ld + n0 + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 t = __ldg(tp + i);
+      f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
+    }
+  }
+  if (p.res.base) {
+    float rv[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      load8(reinterpret_cast<const bf16*>(p.res.base) + rrow + c + 8 * j, rv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[8 * j + i] += rv[i];
+    }
+  }
+}
+
+// Fused GroupNorm statistics of one 32-column chunk held by a warp (lane = row, u = the row's 32
+// bf16 outputs as stored): transpose through smem so lane j sums column j over the 32 rows, then a
+// segmented suffix scan over lanes of the same group; the group's first lane adds into the warp's
+// accumulator sacc[b][g][{sum, sumsq}].  Fixed order everywhere (deterministic).
+__device__ __forceinline__ void gn_chunk_stats(uint32_t* stile, float* sacc, const uint32_t* u, int b, unsigned bmask,
+                                               int col0, int cg) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) stile[lane * 17 + i] = u[i];
+  __syncwarp();
+  const int sh = (lane & 1) * 16, wj = lane >> 1;
+  float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
+  const bool mixed = bmask != 0u && bmask != 0xffffffffu;
+  if (!mixed) {
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const float x = __uint_as_float((stile[rr * 17 + wj] >> sh) << 16);
+      s0 += x; q0 = fmaf(x, x, q0);
+    }
+  } else {
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const float x = __uint_as_float((stile[rr * 17 + wj] >> sh) << 16);
+      if ((bmask >> rr) & 1u) { s1 += x; q1 = fmaf(x, x, q1); } else { s0 += x; q0 = fmaf(x, x, q0); }
+    }
+  }
+  __syncwarp();                                   // stile is rewritten by the next chunk
+  const int col = col0 + lane;
+  const int g = col / cg;
+  const int rem = cg - 1 - (col - g * cg);        // columns after this one in the same group
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const float t0 = __shfl_down_sync(0xffffffffu, s0, d), t1 = __shfl_down_sync(0xffffffffu, q0, d);
+    const float t2 = __shfl_down_sync(0xffffffffu, s1, d), t3 = __shfl_down_sync(0xffffffffu, q1, d);
+    if (d <= rem && lane + d < 32) { s0 += t0; q0 += t1; s1 += t2; q1 += t3; }
+  }
+  if (lane == 0 || rem == cg - 1) {
+    if (!mixed) {
+      float* a = sacc + (b * 32 + g) * 2;
+      a[0] += s0; a[1] += q0;
+    } else {
+      float* a = sacc + g * 2;
+      a[0] += s0; a[1] += q0; a[64] += s1; a[65] += q1;
+    }
+  }
+  __syncwarp();
+}
+
+template <int BN, bool ST>
 __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t tacc, int r, int b, int w, bool valid,
-                                              int n0, int z) {
+                                              int n0, int z, uint32_t* stile, float* sacc, unsigned bmask) {
   const bool second = n0 >= p.n_split;
   const ActView& ov = second ? p.out2 : p.out;
   const int ncol0 = second ? n0 - p.n_split : n0;
@@ -76,35 +161,34 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
       uint32_t v[32];
       sm100::tmem_ld32(tacc + c, v);
       sm100::tmem_wait_ld();
+      if constexpr (ST) {
+        // stats variant (bf16 out, no second output): every lane takes part in the warp transpose
+        uint32_t uo[16];
+        if (valid) {
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+          epilogue_math(p, f, b, rrow, n0, c);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+            uo[i] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          uint4* po = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(ov.base) + orow + c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) po[j] = make_uint4(uo[4 * j], uo[4 * j + 1], uo[4 * j + 2], uo[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) uo[i] = 0u;
+        }
+        gn_chunk_stats(stile, sacc, uo, b, bmask, n0 + c, p.gn_cg);
+        continue;
+      }
       if (!valid || p.epi_skip) continue;
       float f[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-      if (p.bias) {                       // 16-byte vector loads (warp-uniform addresses: L1 broadcast)
-        const float4* bp = reinterpret_cast<const float4*>(p.bias + n0 + c);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 t = __ldg(bp + i);
-          f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
-        }
-      }
-      if (p.temb) {
-        const float4* tp = reinterpret_cast<const float4*>(p.temb + b * p.temb_ld + n0 + c);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 t = __ldg(tp + i);
-          f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
-        }
-      }
-      if (p.res.base) {
-        float rv[8];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          load8(reinterpret_cast<const bf16*>(p.res.base) + rrow + c + 8 * j, rv);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) f[8 * j + i] += rv[i];
-        }
-      }
+      epilogue_math(p, f, b, rrow, n0, c);
       if (ov.dtype == DT_BF16) {
         bf16* po = reinterpret_cast<bf16*>(ov.base) + orow + c;
 #pragma unroll
@@ -118,13 +202,15 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
   }
 }
 
-template <int BN>
+template <int BN, bool ST>
 __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
   // Persistent: CTA c handles work units c, c + gridDim.x, ...; a unit = (m tile, n tile, k split).
   // The smem ring (full/empty) runs continuously across units; two TMEM accumulators (tfull/tempty)
   // let the epilogue of unit i overlap the main loop of unit i+1.
-  using Cfg = TcCfg<BN>;
+  // ST: the epilogue also accumulates the GroupNorm sums of the output (the consumer GN's stats pass
+  // becomes a tiny finalize over gridDim.x * 4 partials).
+  using Cfg = TcCfg<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -134,6 +220,8 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   uint64_t* tfull = empty + Cfg::STAGES;     // [2]
   uint64_t* tempty = tfull + 2;              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* st_tile = reinterpret_cast<uint32_t*>(smem + Cfg::STAGES * Cfg::STAGE + 256);   // ST only
+  float* st_acc = reinterpret_cast<float*>(st_tile + 4 * ST_TILE_WORDS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -218,20 +306,32 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
     const int q = warp & 3;
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
+    uint32_t* stile = st_tile + q * ST_TILE_WORDS;
+    float* sacc = st_acc + q * 128;
+    if (ST) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sacc[lane * 4 + i] = 0.f;
+      __syncwarp();
+    }
     int tc = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tc) {
       int r0, b0, w0, n0, z;
       decode(u, r0, b0, w0, n0, z);
       const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
+      const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
       const int a = tc & 1;
       sm100::mbar_wait(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
       const uint32_t tacc = tmem + a * BN + (uint32_t(q * 32) << 16);
-      gemm_epilogue<BN>(p, tacc, r, b, w, valid, n0, z);
+      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, stile, sacc, bmask);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
+    }
+    if (ST) {
+      const float4 v = *reinterpret_cast<const float4*>(sacc + lane * 4);
+      *reinterpret_cast<float4*>(p.gn_part + ((size_t)blockIdx.x * 4 + q) * 128 + lane * 4) = v;
     }
   }
   sm100::fence_before();
@@ -310,9 +410,12 @@ bool gemm_tc_supported(const GemmArgs& g) {
 }
 
 template <int BN>
-static void launch_bn(const TcGemmParams& p, cudaStream_t s) {
+static int launch_bn(const TcGemmParams& p, cudaStream_t s) {   // returns the grid size
   const int units = p.m_tiles * (p.N / BN) * p.splits;
-  launch_pdl(gemm_tc_kernel<BN>, dim3(units < 148 ? units : 148), dim3(192), TcCfg<BN>::SMEM, s, p);
+  const int grid = units < 148 ? units : 148;
+  if (p.gn_part) launch_pdl(gemm_tc_kernel<BN, true>, dim3(grid), dim3(192), TcCfg<BN, true>::SMEM, s, p);
+  else launch_pdl(gemm_tc_kernel<BN, false>, dim3(grid), dim3(192), TcCfg<BN, false>::SMEM, s, p);
+  return grid;
 }
 
 
@@ -440,7 +543,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
       const int a = tc & 1;
       sm100::mbar_wait_cluster(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
-      gemm_epilogue<BN>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z);
+      gemm_epilogue<BN, false>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, nullptr, nullptr, 0u);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
@@ -512,25 +615,31 @@ void gemm_tc_init() {
   cudaFuncSetAttribute(gemm_tc2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<256>::SMEM);
   cudaFuncSetAttribute(gemm_tc2_kernel<160>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<160>::SMEM);
   cudaFuncSetAttribute(gemm_tc2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<128>::SMEM);
-  cudaFuncSetAttribute(gemm_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
-  cudaFuncSetAttribute(gemm_tc_kernel<160>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<160>::SMEM);
-  cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<128>::SMEM);
-  cudaFuncSetAttribute(gemm_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<64>::SMEM);
+#define PCPP_SMEM_ATTR(BN, ST) \
+  cudaFuncSetAttribute(gemm_tc_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN, ST>::SMEM)
+  PCPP_SMEM_ATTR(256, false); PCPP_SMEM_ATTR(160, false); PCPP_SMEM_ATTR(128, false); PCPP_SMEM_ATTR(64, false);
+  PCPP_SMEM_ATTR(256, true); PCPP_SMEM_ATTR(160, true); PCPP_SMEM_ATTR(128, true); PCPP_SMEM_ATTR(64, true);
+#undef PCPP_SMEM_ATTR
 }
 
 // ---- configuration choice: per-shape autotune cache (filled at plan time), else a heuristic ----
 struct GemmKey {
-  int rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt;
+  int rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt, st;
   bool operator<(const GemmKey& o) const {
-    const int a[11] = {rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt};
-    const int b[11] = {o.rows_out, o.w_out, o.B, o.N, o.cin, o.c0, o.taps, o.stride, o.split_out, o.res, o.odt};
-    for (int i = 0; i < 11; ++i) if (a[i] != b[i]) return a[i] < b[i];
+    const int a[12] = {rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt, st};
+    const int b[12] = {o.rows_out, o.w_out, o.B, o.N, o.cin, o.c0, o.taps, o.stride, o.split_out, o.res, o.odt, o.st};
+    for (int i = 0; i < 12; ++i) if (a[i] != b[i]) return a[i] < b[i];
     return false;
   }
 };
+// GroupNorm statistics can ride on the epilogue of a single-output bf16 GEMM (no split-K, 1-CTA)
+static bool gn_fusable(const GemmArgs& g) {
+  return g.gn_part && g.gn_slots && g.out.dtype == DT_BF16 && !g.out2.base && g.n_split >= g.N && g.N % 32 == 0 &&
+         (g.N / 32) >= 2;
+}
 static GemmKey key_of(const GemmArgs& g) {
   return GemmKey{g.rows_out, g.w_out, g.B, g.N, g.cin, g.c0, g.taps, g.stride, g.n_split < g.N ? g.n_split : 0,
-                 g.res.base ? 1 : 0, g.out.dtype};
+                 g.res.base ? 1 : 0, g.out.dtype, gn_fusable(g) ? 1 : 0};
 }
 struct GemmChoice { int bn, splits, pair; };
 static std::map<GemmKey, GemmChoice>& tune_cache() { static std::map<GemmKey, GemmChoice> m; return m; }
@@ -567,6 +676,8 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   const int nsteps = p.taps * p.nkc;
   const long long M = (long long)g.rows_out * g.B * g.w_out;
   p.splits = 1; p.s_len = nsteps; p.ws = g.ws;
+  const bool st = gn_fusable(g);
+  if (st) { want_splits = 1; pair = 0; p.gn_part = g.gn_part; p.gn_cg = g.N / 32; }
   if (want_splits > 1 && g.ws && (size_t)want_splits * M * g.N <= g.ws_elems) {
     p.s_len = (nsteps + want_splits - 1) / want_splits;
     p.splits = (nsteps + p.s_len - 1) / p.s_len;
@@ -580,12 +691,14 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
       default: launch_bn2<128>(p, s); break;
     }
   } else {
+    int grid = 0;
     switch (BN) {
-      case 256: launch_bn<256>(p, s); break;
-      case 160: launch_bn<160>(p, s); break;
-      case 128: launch_bn<128>(p, s); break;
-      default: launch_bn<64>(p, s); break;
+      case 256: grid = launch_bn<256>(p, s); break;
+      case 160: grid = launch_bn<160>(p, s); break;
+      case 128: grid = launch_bn<128>(p, s); break;
+      default: grid = launch_bn<64>(p, s); break;
     }
+    if (st) *g.gn_slots = 4 * grid;
   }
   if (p.splits > 1) {
     const long long total = M * (g.N / 8);
@@ -656,8 +769,9 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
   for (int bn : bns) {
     if (!bn_ok(g, bn)) continue;
     if (pair && bn == 64) continue;
+    if (pair && gn_fusable(g)) continue;
     for (int S = 1; S <= 6; ++S) {
-      if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems)) break;
+      if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems || gn_fusable(g))) break;
       if (!launch_gemm_tc_cfg(g, s, bn, S, pair)) continue;      // warm
       cudaEventRecord(e0, s);
       for (int r = 0; r < 3; ++r) launch_gemm_tc_cfg(g, s, bn, S, pair);

@@ -157,6 +157,34 @@ void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
   else launch_pdl(gn_stats_kernel<bf16>, dim3(a.nchunk), dim3(NT), smem, s, a);
 }
 
+// ---- finalize of the GEMM-fused statistics ------------------------------------------------------
+// CTA (b, g): 128 threads stride over the slots in fp64, then a fixed-order tree.
+__global__ void __launch_bounds__(128) gn_finalize_kernel(const float* __restrict__ part, int nslots,
+                                                          double* __restrict__ m_out) {
+  pdl_trigger();
+  pdl_wait();
+  const int i = blockIdx.x;                  // b * G + g
+  double s = 0.0, q = 0.0;
+  for (int k = threadIdx.x; k < nslots; k += 128) {
+    const float2 v = __ldcg(reinterpret_cast<const float2*>(part + (size_t)k * 128) + i);
+    s += v.x; q += v.y;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) { s += __shfl_xor_sync(0xffffffffu, s, d); q += __shfl_xor_sync(0xffffffffu, q, d); }
+  __shared__ double red[4][2];
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[warp][0] = s; red[warp][1] = q; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    m_out[2 * i] = (red[0][0] + red[1][0]) + (red[2][0] + red[3][0]);
+    m_out[2 * i + 1] = (red[0][1] + red[1][1]) + (red[2][1] + red[3][1]);
+  }
+}
+
+void launch_gn_finalize(const float* part, int nslots, double* m_out, cudaStream_t s) {
+  launch_pdl(gn_finalize_kernel, dim3(2 * G), dim3(128), 0, s, part, nslots, m_out);
+}
+
 // ---- apply -------------------------------------------------------------------------------------
 __device__ __forceinline__ void gn_prep(const GnApplyArgs& a, float* mu_s, float* rs_s) {
   const int B = a.x0.B;

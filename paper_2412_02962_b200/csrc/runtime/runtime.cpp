@@ -67,6 +67,21 @@ pcpp_status plan_allocate(Plan& P) {
     g.off_part = off; off = align256(off + (size_t)B_CFG * g.nchunk * GN_G * 2 * sizeof(double));
     g.off_cnt = off; off = align256(off + 16);
   }
+  // GN statistics fused into the producing GEMM's epilogue (bf16 tensor-core path): the GN reads
+  // x0 only, and x0's last writer is a CONV/GEMM that writes nothing else
+  static const int gn_fuse_env = getenv("PCPP_GN_FUSE") ? atoi(getenv("PCPP_GN_FUSE")) : 1;
+  for (size_t i = 0; i < P.ops.size(); ++i) {
+    Op& o = P.ops[i];
+    if (o.k != OP_GN || o.in1 >= 0 || !gn_fuse_env || P.dtype != DT_BF16) continue;
+    for (size_t j = i; j-- > 0;) {
+      Op& pr = P.ops[j];
+      if (pr.out != o.in0 && pr.out2 != o.in0) continue;
+      if ((pr.k == OP_CONV || pr.k == OP_GEMM) && pr.out == o.in0 && pr.out2 < 0 && pr.gn_fuse < 0) pr.gn_fuse = o.xid;
+      break;
+    }
+  }
+  P.off_epart = off; off = align256(off + (size_t)148 * 4 * 128 * sizeof(float));
+  P.gn_slots.assign((size_t)P.nr * P.gns.size(), 0);
   const size_t es = dtype_size(P.dtype);
   size_t gat_level[3] = {0, 0, 0};
   bool have_level[3] = {false, false, false};
@@ -434,6 +449,8 @@ pcpp_status plan_autotune(Plan& P) {
     g.out = o;
     if (op.out2 >= 0) { g.out2 = view(P, 0, op.out2, 0); g.n_split = op.n_split; }
     g.ws = P.ws; g.ws_elems = P.ws_elems;
+    int slots = 0;
+    if (op.gn_fuse >= 0) { g.gn_part = reinterpret_cast<float*>(P.rm[0].arena + P.off_epart); g.gn_slots = &slots; }
     if (gemm_tc_supported(g)) gemm_tc_autotune(g, P.s0);
   }
   CK(cudaStreamSynchronize(P.s0));
@@ -495,6 +512,10 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           g.out = o;
           if (op.out2 >= 0) { g.out2 = view(P, vr, op.out2, par); g.n_split = op.n_split; }
           g.ws = P.ws; g.ws_elems = P.ws_elems;
+          if (op.gn_fuse >= 0) {
+            g.gn_part = reinterpret_cast<float*>(P.rm[vr].arena + P.off_epart);
+            g.gn_slots = &P.gn_slots[(size_t)vr * P.gns.size() + op.gn_fuse];
+          }
           launch_gemm_tc_or_simt(P, g, s);
         }
         P.launches_per_step += nr;
@@ -531,7 +552,14 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           return a;
         };
         {
-          for (int vr = 0; vr < nr && do_op; ++vr) launch_gn_stats(stats_args(vr), s);
+          for (int vr = 0; vr < nr && do_op; ++vr) {
+            const int slots = P.gn_slots[(size_t)vr * P.gns.size() + op.xid];
+            if (slots > 0)
+              launch_gn_finalize(reinterpret_cast<const float*>(P.rm[vr].arena + P.off_epart), slots,
+                                 reinterpret_cast<double*>(P.rm[vr].arena + gx.off_m[par]), s);
+            else
+              launch_gn_stats(stats_args(vr), s);
+          }
           if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
           for (int vr = 0; vr < nr && do_op; ++vr) launch_gn_apply(apply_args(vr), s);
           P.launches_per_step += 2 * nr;

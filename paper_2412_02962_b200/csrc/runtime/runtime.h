@@ -39,6 +39,7 @@ struct Op {
   int temb_off = -1;        // column offset into tproj [2][J]
   int xid = -1;             // exchange id (halo / gn / attn index)
   int N = 0;                // output channels for GEMM/CONV
+  int gn_fuse = -1;         // GEMM/CONV: GroupNorm index whose statistics its epilogue produces
 };
 
 // ---- exchange buffers --------------------------------------------------------------------------
@@ -99,6 +100,8 @@ struct Plan {
 
   // per-rank memory
   size_t rank_bytes = 0;
+  size_t off_epart = 0;                 // per-rank GEMM-fused GN statistics partials
+  std::vector<int> gn_slots;            // [nr][ngn]: slots the producer GEMM wrote (0: not fused)
   std::vector<RankMem> rm;
   // global memory
   void* wmat = nullptr;  float* wf32 = nullptr;
