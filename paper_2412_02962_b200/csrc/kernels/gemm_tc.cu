@@ -425,20 +425,23 @@ static int launch_bn(const TcGemmParams& p, cudaStream_t s) {   // returns the g
 // so per-SM smem traffic per MMA cycle drops by ~30% and the ring gets deeper -- the 1-CTA kernel
 // is TMA-latency bound (profiles/r1_ncu_gemm_*).
 // ---------------------------------------------------------------------------------------------
-template <int BN>
+template <int BN, bool ST = false>
 struct TcCfg2 {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = (BN / 2) * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (223232 / STAGE) > 10 ? 10 : (223232 / STAGE);
+  static constexpr int RING = 223232 - (ST ? ST_SMEM : 0);
+  static constexpr int STAGES = (RING / STAGE) > 10 ? 10 : (RING / STAGE);
   static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + (ST ? ST_SMEM : 0);
 };
 
-template <int BN>
+// ST: the epilogue also accumulates the GroupNorm sums of the output (as the 1-CTA kernel); each
+// CTA of the pair owns its 128 rows, so the per-warp partial slots are blockIdx.x * 4 + warp.
+template <int BN, bool ST>
 __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
-  using Cfg = TcCfg2<BN>;
+  using Cfg = TcCfg2<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -448,6 +451,8 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
   uint64_t* tfull = empty + Cfg::STAGES;     // [2]
   uint64_t* tempty = tfull + 2;              // [2] (leader's counts both CTAs' epilogue warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* st_tile = reinterpret_cast<uint32_t*>(smem + Cfg::STAGES * Cfg::STAGE + 256);   // ST only
+  float* st_acc = reinterpret_cast<float*>(st_tile + 4 * ST_TILE_WORDS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_rank();
@@ -534,19 +539,31 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
     const int q = warp & 3;
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
+    uint32_t* stile = st_tile + q * ST_TILE_WORDS;
+    float* sacc = st_acc + q * 128;
+    if (ST) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sacc[lane * 4 + i] = 0.f;
+      __syncwarp();
+    }
     int tc = 0;
     for (int u = cid; u < units; u += ncl, ++tc) {
       int r0, b0, w0, n0, z;
       decode(u, r0, b0, w0, n0, z);
       const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
+      const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
       const int a = tc & 1;
       sm100::mbar_wait_cluster(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
-      gemm_epilogue<BN, false>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, nullptr, nullptr, 0u);
+      gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, stile, sacc, bmask);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
+    }
+    if (ST) {
+      const float4 v = *reinterpret_cast<const float4*>(sacc + lane * 4);
+      *reinterpret_cast<float4*>(p.gn_part + ((size_t)blockIdx.x * 4 + q) * 128 + lane * 4) = v;
     }
   }
   sm100::fence_before();
@@ -555,18 +572,22 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
 }
 
 template <int BN>
-static void launch_bn2(const TcGemmParams& p, cudaStream_t s) {
+static int launch_bn2(const TcGemmParams& p, cudaStream_t s) {   // returns the grid size (CTAs)
   const int units = ((p.m_tiles + 1) / 2) * (p.N / BN) * p.splits;
   const int clusters = units < 74 ? units : 74;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(192); cfg.dynamicSmemBytes = TcCfg2<BN>::SMEM; cfg.stream = s;
+  const bool st = p.gn_part != nullptr;
+  cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = st ? TcCfg2<BN, true>::SMEM : TcCfg2<BN, false>::SMEM; cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at; cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN>, p);
+  if (st) cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, true>, p);
+  else cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, false>, p);
+  return 2 * clusters;
 }
 
 // split-K epilogue: out[T][n] = sum_z ws[z][T][n] (fixed order) + bias + temb + residual
@@ -612,9 +633,11 @@ static double wave_eff(long long ctas) {
 }
 
 void gemm_tc_init() {
-  cudaFuncSetAttribute(gemm_tc2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<256>::SMEM);
-  cudaFuncSetAttribute(gemm_tc2_kernel<160>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<160>::SMEM);
-  cudaFuncSetAttribute(gemm_tc2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<128>::SMEM);
+#define PCPP_SMEM_ATTR2(BN, ST) \
+  cudaFuncSetAttribute(gemm_tc2_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg2<BN, ST>::SMEM)
+  PCPP_SMEM_ATTR2(256, false); PCPP_SMEM_ATTR2(160, false); PCPP_SMEM_ATTR2(128, false);
+  PCPP_SMEM_ATTR2(256, true); PCPP_SMEM_ATTR2(160, true); PCPP_SMEM_ATTR2(128, true);
+#undef PCPP_SMEM_ATTR2
 #define PCPP_SMEM_ATTR(BN, ST) \
   cudaFuncSetAttribute(gemm_tc_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN, ST>::SMEM)
   PCPP_SMEM_ATTR(256, false); PCPP_SMEM_ATTR(160, false); PCPP_SMEM_ATTR(128, false); PCPP_SMEM_ATTR(64, false);
@@ -677,7 +700,7 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   const long long M = (long long)g.rows_out * g.B * g.w_out;
   p.splits = 1; p.s_len = nsteps; p.ws = g.ws;
   const bool st = gn_fusable(g);
-  if (st) { want_splits = 1; pair = 0; p.gn_part = g.gn_part; p.gn_cg = g.N / 32; }
+  if (st) { want_splits = 1; p.gn_part = g.gn_part; p.gn_cg = g.N / 32; }
   if (want_splits > 1 && g.ws && (size_t)want_splits * M * g.N <= g.ws_elems) {
     p.s_len = (nsteps + want_splits - 1) / want_splits;
     p.splits = (nsteps + p.s_len - 1) / p.s_len;
@@ -685,11 +708,13 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   if (pair) {
     // B box carries BN/2 rows per CTA
     if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN / 2)) return false;
+    int grid = 0;
     switch (BN) {
-      case 256: launch_bn2<256>(p, s); break;
-      case 160: launch_bn2<160>(p, s); break;
-      default: launch_bn2<128>(p, s); break;
+      case 256: grid = launch_bn2<256>(p, s); break;
+      case 160: grid = launch_bn2<160>(p, s); break;
+      default: grid = launch_bn2<128>(p, s); break;
     }
+    if (st) *g.gn_slots = 4 * grid;
   } else {
     int grid = 0;
     switch (BN) {
@@ -769,7 +794,6 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
   for (int bn : bns) {
     if (!bn_ok(g, bn)) continue;
     if (pair && bn == 64) continue;
-    if (pair && gn_fusable(g)) continue;
     for (int S = 1; S <= 6; ++S) {
       if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems || gn_fusable(g))) break;
       if (!launch_gemm_tc_cfg(g, s, bn, S, pair)) continue;      // warm
@@ -783,6 +807,14 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
     }
   }
   cudaEventDestroy(e0); cudaEventDestroy(e1);
+  static const int log = getenv("PCPP_GEMM_LOG") ? atoi(getenv("PCPP_GEMM_LOG")) : 0;
+  if (log) {
+    const double fl = 2.0 * M * g.N * g.taps * g.cin;
+    fprintf(stderr, "gemm-tune rows=%d w=%d N=%d cin=%d taps=%d stride=%d res=%d gn=%d out2=%d -> bn=%d splits=%d pair=%d  "
+            "%.1f us  %.0f TF/s\n", g.rows_out, g.w_out, g.N, g.cin, g.taps, g.stride, g.res.base ? 1 : 0,
+            gn_fusable(g) ? 1 : 0, g.out2.base ? 1 : 0, best.bn, best.splits, best.pair, best_ms / 3 * 1e3,
+            fl / (best_ms / 3 * 1e-3) / 1e12);
+  }
   std::lock_guard<std::mutex> lk(tune_mu());
   tune_cache()[key] = best;
 }

@@ -102,6 +102,37 @@ def test_attention_sources(cuda_ok, dtype, impl, geo):
     assert rel(back(out), ref) <= TOL[dtype] / (10 if dtype == "fp32" else 2)
 
 
+@pytest.mark.parametrize("geo", [(16, 64, 640, (6, 16, 6)), (8, 128, 128, (0, 8, 3)), (1, 32, 64, (0, 1, 0))])
+def test_attention_split_ranges_deterministic(cuda_ok, geo):
+    """The tcgen05 kernel cuts the (query-tile pair, key tile) space into per-SM ranges and combines
+    split pairs in CTA order: repeated launches are bit-identical (the arrival counters reset) and
+    match the softmax definition."""
+    import torch
+    h, W, Cm, rows = geo
+    rng = np.random.default_rng(5)
+    qx = q(rng.standard_normal((h, 2, W, Cm)), "bf16")
+    srcs = [q(rng.standard_normal((r, 2, W, 2 * Cm)) * 2.0, "bf16") for r in rows if r > 0]
+    kv_rows = [r for r in rows if r > 0]
+    kvs = [T(s, "bf16") for s in srcs]
+    outs = []
+    for _ in range(3):
+        out = torch.empty((h, 2, W, Cm), device="cuda", dtype=torch.bfloat16)
+        pcpp.pcpp_op_attention(T(qx, "bf16"), kvs, kv_rows, h, 2, W, Cm, out, impl="auto")
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    K = np.concatenate([s[..., :Cm] for s in srcs], axis=0)
+    V = np.concatenate([s[..., Cm:] for s in srcs], axis=0)
+    ref = np.zeros((h, 2, W, Cm))
+    for b in range(2):
+        Qb = qx[:, b].reshape(-1, Cm); Kb = K[:, b].reshape(-1, Cm); Vb = V[:, b].reshape(-1, Cm)
+        for hd in range(Cm // 64):
+            sl = slice(hd * 64, hd * 64 + 64)
+            Pm = M._softmax_rows(Qb[:, sl] @ Kb[:, sl].T / 8.0)
+            ref[:, b, :, sl] = (Pm @ Vb[:, sl]).reshape(h, W, 64)
+    assert rel(back(outs[0]), ref) <= 1e-2
+
+
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 @pytest.mark.parametrize("shape", [(16, 32, 320), (3, 24, 640), (64, 64, 128), (2, 32, 2560)])
 def test_groupnorm(cuda_ok, dtype, shape):

@@ -138,3 +138,22 @@ def test_sample_e2e_host_buffers(cuda_ok):
     plan.close()
     np.testing.assert_array_equal(x0, x0b)       # deterministic, reset works
     assert rel_l2(x0, oracle_run(*case)[-1]) <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("force", ["160,1,1", "128,1,1", "256,1,1", "160,1,0", "64,1,0", "128,3,0"])
+def test_forced_gemm_configs(cuda_ok, force, tmp_path):
+    """Every tcgen05 GEMM variant the autotuner can pick (1-CTA / 2-CTA pair, BN, split-K, with and
+    without the fused GroupNorm statistics) reproduces the oracle on the SDXL-shaped stack."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "xs.npy"
+    env = dict(os.environ, PCPP_GEMM_FORCE=force)
+    r = subprocess.run([sys.executable, "-m", "tests._force_run", str(out)], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    xs = np.load(out)
+    ref = oracle_run("sdxl", 32, 1, 0.0, 0, 50, "bf16", "pcpp", 2)
+    for k in range(2):
+        assert rel_l2(xs[k], ref[k]) <= TOL["bf16"], (force, k)
