@@ -7,6 +7,7 @@
 // owns fixed 8-channel vectors (16 B) of every token it visits, so its gamma/beta and group ids are
 // registers and each warp reads contiguous 16 B vectors of one token row (coalesced).
 // Deterministic: fixed-order reductions only (loopback == NCCL bitwise, graph == eager bitwise).
+#include <cstdlib>
 #include "../common.cuh"
 #include "../kernels.h"
 
@@ -334,7 +335,84 @@ void launch_gn_fused(const GnStatsArgs& sa, const GnApplyArgs& aa, cudaStream_t 
   else launch_pdl(gn_fused_kernel<bf16, bf16>, dim3(a2.nchunk), dim3(NT), smem, s, a2, aa);
 }
 
+// Wide apply: every thread of the grid owns one fixed 8-channel vector lane v = gid % nv (so its
+// affine coefficients for both CFG branches live in registers) and walks the tokens t = gid / nv,
+// + lanes, ... (lanes = threads / nv); consecutive threads read consecutive 16-byte vectors of a
+// token row (coalesced) and each keeps 4 independent loads in flight.  One wave of <= 2 CTAs/SM, so
+// the statistics prologue is paid once per CTA.
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a, int lanes) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float mu_s[2 * G], rs_s[2 * G];
+  const int B = a.x0.B, C = a.C, cg = C / G, nv = C / 8, W = a.x0.W;
+  gn_prep(a, mu_s, rs_s);
+  __syncthreads();
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= lanes * nv) return;
+  const int v = gid % nv;
+  const int c = v * 8;
+  float A[2][8], Bc[2][8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int g = (c + e) / cg;
+    const float ga = a.gamma[c + e], be = a.beta[c + e];
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      const int bi = bb < B ? bb : 0;
+      const float rs = rs_s[bi * G + g] * ga;
+      A[bb][e] = rs;
+      Bc[bb][e] = be - mu_s[bi * G + g] * rs;
+    }
+  }
+  const bool second = a.x1.base != nullptr && c >= a.c0;
+  const TI* src = reinterpret_cast<const TI*>(second ? a.x1.base : a.x0.base) + (second ? c - a.c0 : c);
+  const int sC = second ? a.x1.C : a.x0.C;
+  TO* dst = reinterpret_cast<TO*>(a.out.base) + c;
+  const int ntok = a.x0.rows * B * W;
+  for (int t0 = gid / nv; t0 < ntok; t0 += 4 * lanes) {
+    float x[4][8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = t0 + k * lanes;
+      if (t < ntok) load8(src + (long long)t * sC, x[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = t0 + k * lanes;
+      if (t >= ntok) continue;
+      const int bb = (t / W) % B;
+      float* xv = x[k];
+      if (bb) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[e] = fmaf(xv[e], A[1][e], Bc[1][e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[e] = fmaf(xv[e], A[0][e], Bc[0][e]);
+      }
+      if (a.silu) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[e] = silu_f(xv[e]);
+      }
+      store8(dst + (long long)t * a.out.C, xv);
+    }
+  }
+}
+
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
+  static const int wide = getenv("PCPP_GN_WIDE") ? atoi(getenv("PCPP_GN_WIDE")) : 1;
+  if (wide && a.C % 8 == 0 && a.x0.B <= 2 && (a.x1.base == nullptr || a.c0 % 8 == 0)) {
+    const int nv = a.C / 8;
+    const long long ntok = (long long)a.x0.rows * a.x0.B * a.x0.W;
+    long long blocks = (ntok * nv + 512 * 4 - 1) / (512 * 4);
+    if (blocks > 148 * 2) blocks = 148 * 2;
+    if (blocks < 1) blocks = 1;
+    int lanes = (int)(blocks * 512 / nv);
+    if (lanes < 1) { lanes = 1; blocks = (nv + 511) / 512; }
+    if (a.x0.dtype == DT_F32) launch_pdl(gn_apply_wide_kernel<float, float>, dim3((unsigned)blocks), dim3(512), 0, s, a, lanes);
+    else launch_pdl(gn_apply_wide_kernel<bf16, bf16>, dim3((unsigned)blocks), dim3(512), 0, s, a, lanes);
+    return;
+  }
   const Lanes L = lanes_for(a.C);
   const long long ntok = (long long)a.x0.rows * a.x0.B * a.x0.W;
   long long per = (long long)L.ntl * 8;                           // ~8 tokens per token lane
