@@ -232,6 +232,8 @@ def main():
 
     # per-kind breakdown of one async step, each kind captured alone (pcpp_profile)
     prof = {}
+    if os.environ.get("PCPP_OP_TIMING"):          # per-op device-time table on stderr (tuning aid)
+        plan.pcpp_profile(lat, 31, 0, 1)
     if not args.no_profile:
         for name, mask in (("conv_gemm", 1), ("attention", 2), ("groupnorm", 4), ("exchange", 8), ("other", 16)):
             prof[name] = plan.pcpp_profile(lat, mask, 0, 5)

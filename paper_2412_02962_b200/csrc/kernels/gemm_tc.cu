@@ -56,7 +56,7 @@ struct TcCfg {
 // epilogue of one 128 x BN accumulator tile held in TMEM (this thread = one row): bias + temb +
 // residual -> bf16/fp32 store, or raw fp32 partials for split-K
 // bias + temb + residual for one row's 32-column chunk starting at column n0 + c
-__device__ __forceinline__ void epilogue_math(const TcGemmParams& p, float* f, int b, long long rrow, int n0, int c) {
+__device__ __forceinline__ void epilogue_math(const TcGemmParams& p, float* f, int b, const uint4* rres, int n0, int c) {
   if (p.bias) {                       // 16-byte vector loads (warp-uniform addresses: L1 broadcast)
     const float4* bp = reinterpret_cast<const float4*>(p.bias + n0 + c);
 #pragma unroll
@@ -73,14 +73,24 @@ __device__ __forceinline__ void epilogue_math(const TcGemmParams& p, float* f, i
       f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
     }
   }
-  if (p.res.base) {
-    float rv[8];
+  if (p.res.base) {                   // residual chunk, prefetched by the caller (rres = 32 bf16)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      load8(reinterpret_cast<const bf16*>(p.res.base) + rrow + c + 8 * j, rv);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&rres[j]);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) f[8 * j + i] += rv[i];
+      for (int i = 0; i < 4; ++i) {
+        const float2 t = __bfloat1622float2(h[i]);
+        f[8 * j + 2 * i] += t.x; f[8 * j + 2 * i + 1] += t.y;
+      }
     }
+  }
+}
+// residual chunk [c, c+32) of this row (4 x 16 B); issued one chunk ahead of its use
+__device__ __forceinline__ void res_prefetch(const TcGemmParams& p, long long rrow, int c, bool valid, uint4* rres) {
+  if (p.res.base && valid) {
+    const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(p.res.base) + rrow + c);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) rres[j] = __ldg(rp + j);
   }
 }
 
@@ -132,14 +142,21 @@ __device__ __forceinline__ void gn_chunk_stats(uint32_t* stile, float* sacc, con
   __syncwarp();
 }
 
+__device__ __forceinline__ long long res_row(const TcGemmParams& p, int r, int b, int w, int n0) {
+  return p.res.base ? (((long long)r * p.res.B + b) * p.res.W + w) * p.res.C + n0 : 0;
+}
+
+// rres0: the residual of chunk 0, prefetched by the caller before it waited for the accumulator
 template <int BN, bool ST>
 __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t tacc, int r, int b, int w, bool valid,
-                                              int n0, int z, uint32_t* stile, float* sacc, unsigned bmask) {
+                                              int n0, int z, uint32_t* stile, float* sacc, unsigned bmask,
+                                              const uint4* rres0) {
   const bool second = n0 >= p.n_split;
   const ActView& ov = second ? p.out2 : p.out;
   const int ncol0 = second ? n0 - p.n_split : n0;
   const long long orow = (((long long)r * ov.B + b) * ov.W + w) * ov.C + ncol0;
-  const long long rrow = p.res.base ? (((long long)r * p.res.B + b) * p.res.W + w) * p.res.C + n0 : 0;
+  const long long rrow = res_row(p, r, b, w, n0);
+  uint4 rcur[4] = {rres0[0], rres0[1], rres0[2], rres0[3]}, rnext[4];
   if (p.splits > 1) {
     // split-K: raw fp32 partial tile -> workspace; gemm_splitk_finish applies the epilogue
     const long long T = ((long long)r * p.B + b) * p.w_out + w;
@@ -158,6 +175,7 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
   } else {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
+      if (c + 32 < BN) res_prefetch(p, rrow, c + 32, valid, rnext);
       uint32_t v[32];
       sm100::tmem_ld32(tacc + c, v);
       sm100::tmem_wait_ld();
@@ -168,7 +186,7 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
           float f[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-          epilogue_math(p, f, b, rrow, n0, c);
+          epilogue_math(p, f, b, rcur, n0, c);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
@@ -182,13 +200,17 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
           for (int i = 0; i < 16; ++i) uo[i] = 0u;
         }
         gn_chunk_stats(stile, sacc, uo, b, bmask, n0 + c, p.gn_cg);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rcur[j] = rnext[j];
         continue;
       }
       if (!valid || p.epi_skip) continue;
       float f[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-      epilogue_math(p, f, b, rrow, n0, c);
+      epilogue_math(p, f, b, rcur, n0, c);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) rcur[j] = rnext[j];
       if (ov.dtype == DT_BF16) {
         bf16* po = reinterpret_cast<bf16*>(ov.base) + orow + c;
 #pragma unroll
@@ -320,11 +342,13 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
       const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
+      uint4 rres0[4];
+      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), 0, valid, rres0);   // overlaps the main loop
       const int a = tc & 1;
       sm100::mbar_wait(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
       const uint32_t tacc = tmem + a * BN + (uint32_t(q * 32) << 16);
-      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, stile, sacc, bmask);
+      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, stile, sacc, bmask, rres0);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
@@ -553,10 +577,12 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
       const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
       const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
+      uint4 rres0[4];
+      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), 0, valid, rres0);
       const int a = tc & 1;
       sm100::mbar_wait_cluster(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
-      gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, stile, sacc, bmask);
+      gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, stile, sacc, bmask, rres0);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));

@@ -350,6 +350,8 @@ pcpp_status pcpp_profile(pcpp_plan_t h, float* latent, int kind, int sync, int i
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge = nullptr;
   CKS(cudaStreamSynchronize(P.s0));
+  static const int op_timing = getenv("PCPP_OP_TIMING") ? atoi(getenv("PCPP_OP_TIMING")) : 0;
+  if (op_timing && kind == 31 && !fork) { print_op_timing(P, latent, sync, P.k & 1); CKS(cudaStreamSynchronize(P.s0)); }
   CKS(cudaStreamBeginCapture(P.s0, cudaStreamCaptureModeRelaxed));
   if (fork) { cudaEventRecord(P.ev_fork, P.s0); cudaStreamWaitEvent(P.s1, P.ev_fork, 0); }
   pcpp_status st = run_step(P, latent, sync, P.k & 1, (unsigned)kind);

@@ -465,6 +465,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
   const size_t es = dtype_size(P.dtype);
   const char* wm = reinterpret_cast<const char*>(P.wmat);
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
+    if (P.op_ev_on) cudaEventRecord(P.op_ev[oi], s);
     const Op& op = P.ops[oi];
     const int xo_all = P.op_xord[oi];
     const unsigned kind = op_kind(op.k);
@@ -625,8 +626,43 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
         break;
     }
   }
+  if (P.op_ev_on) cudaEventRecord(P.op_ev[P.ops.size()], s);
   CK(cudaGetLastError());
   return PCPP_OK;
+}
+
+// Per-op device time of one eager step (events between ops; the host runs ahead of the device for
+// every op longer than the launch latency), printed to stderr.  Debug / tuning aid only.
+void print_op_timing(Plan& P, float* latent, int sync, int par) {
+  const size_t n = P.ops.size() + 1;
+  P.op_ev.resize(n);
+  for (auto& e : P.op_ev) cudaEventCreate(&e);
+  P.op_ev_on = true;
+  for (int rep = 0; rep < 2; ++rep) run_step(P, latent, sync, par, ~0u);
+  cudaStreamSynchronize(P.s0);
+  P.op_ev_on = false;
+  static const char* names[] = {"TEMB", "PREP", "HALO", "CONV", "GEMM", "GN", "KVX", "ATTN", "UPS", "COUT", "CFG", "END"};
+  double tot = 0;
+  for (size_t oi = 0; oi + 1 < n; ++oi) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, P.op_ev[oi], P.op_ev[oi + 1]);
+    tot += ms;
+    const Op& op = P.ops[oi];
+    const int k = (int)op.k;
+    if (op.k == OP_CONV || op.k == OP_GEMM) {
+      const TDesc& o = P.td[op.out];
+      const int cin = P.td[op.in0].C + (op.in1 >= 0 ? P.td[op.in1].C : 0);
+      const double fl = 2.0 * o.rows * B_CFG * o.W * op.N * (op.k == OP_CONV ? 9 : 1) * cin * P.nr;
+      fprintf(stderr, "op %3zu %-4s rows=%3d W=%3d N=%4d cin=%4d s=%d res=%d gn=%d out2=%d %8.1f us %6.0f TF/s\n", oi,
+              names[k], o.rows, o.W, op.N, cin, op.stride, op.res >= 0, op.gn_fuse >= 0, op.out2 >= 0, ms * 1e3,
+              fl / (ms * 1e-3) / 1e12);
+    } else {
+      fprintf(stderr, "op %3zu %-4s %8.1f us\n", oi, k >= 0 && k < 12 ? names[k] : "?", ms * 1e3);
+    }
+  }
+  fprintf(stderr, "op-timing total %.3f ms\n", tot);
+  for (auto& e : P.op_ev) cudaEventDestroy(e);
+  P.op_ev.clear();
 }
 
 void op_work(const Plan& P, unsigned kind, int sync, double* flops, double* bytes, int* launches) {

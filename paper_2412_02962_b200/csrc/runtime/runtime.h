@@ -108,6 +108,7 @@ struct Plan {
   float* emb = nullptr; float* hid = nullptr; float* tproj = nullptr; float* cond = nullptr;
   int* taus = nullptr; double* coef = nullptr; int* k_dev = nullptr;
   float* ws = nullptr; size_t ws_elems = 0;   // split-K workspace
+  std::vector<cudaEvent_t> op_ev; bool op_ev_on = false;   // per-op timing (PCPP_OP_TIMING, pcpp_profile)
   std::vector<void*> gallocs;
 
   // exchange descriptors: [sync][par] per exchange op index
@@ -145,6 +146,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask = 
 // algorithmic work of the ops of one kind in one step (all virtual ranks): flops, bytes, launches
 void op_work(const Plan& P, unsigned kind, int sync, double* flops, double* bytes, int* launches);
 int band_rows(double p, int h);
+void print_op_timing(Plan& P, float* latent, int sync, int par);
 const char* set_error(const char* fmt, ...);
 
 // kernels init
