@@ -156,7 +156,23 @@ def run_reference(args):
     return 0
 
 
+def _progress(msg):
+    """Phase marker on stderr (the JSON line stays the only stdout line)."""
+    if os.environ.get("PCPP_BENCH_QUIET") is None:
+        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+TUNE_FILE = os.path.join(ROOT, "profiles", "gemm_tune_b200.txt")
+
+
 def main():
+    # GEMM configurations: the committed per-shape table (deterministic across runs and identical
+    # under ncu); shapes it lacks are tuned at plan time
+    if os.path.exists(TUNE_FILE):
+        os.environ.setdefault("PCPP_TUNE_FILE", TUNE_FILE)
+    import faulthandler
+    # a wedged run dumps every thread's stack and exits instead of hanging the caller
+    faulthandler.dump_traceback_later(int(os.environ.get("PCPP_BENCH_WATCHDOG_S", "900")), exit=True)
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -200,6 +216,7 @@ def main():
     if plan is None:
         raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
     del blob
+    _progress("plan built (weights uploaded, GEMMs autotuned, graphs pending)")
     plan.pcpp_set_cond(cond)
     patch = xT[rank * h:(rank + 1) * h] if world > 1 else xT
     lat = torch.from_numpy(np.ascontiguousarray(patch)).cuda()
@@ -213,6 +230,7 @@ def main():
     for k in range(pre):
         plan.pcpp_step(lat, k)
     torch.cuda.synchronize()
+    _progress("warm-up steps done")
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -223,6 +241,7 @@ def main():
         ev1.record()
         torch.cuda.synchronize()
     barrier()
+    _progress("timed steps done")
     ms = ev0.elapsed_time(ev1) / args.steps
     if dist is not None:
         t = torch.tensor([ms], device="cuda")

@@ -799,6 +799,31 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   return launch_gemm_tc_cfg(g, s, c.bn, c.splits, c.pair);
 }
 
+// Persisted tuning table (PCPP_TUNE_FILE): one line per shape key -> (bn, splits, pair).  Loading it
+// makes the configuration choice deterministic across runs (and identical under a profiler, whose
+// serialisation would distort the plan-time timing); gemm_tune_save writes the current table.
+void gemm_tune_load(const char* path) {
+  FILE* f = fopen(path, "r");
+  if (!f) return;
+  std::lock_guard<std::mutex> lk(tune_mu());
+  GemmKey k; GemmChoice c;
+  while (fscanf(f, "%d %d %d %d %d %d %d %d %d %d %d %d %d %d %d", &k.rows_out, &k.w_out, &k.B, &k.N, &k.cin, &k.c0,
+                &k.taps, &k.stride, &k.split_out, &k.res, &k.odt, &k.st, &c.bn, &c.splits, &c.pair) == 15)
+    tune_cache()[k] = c;
+  fclose(f);
+}
+void gemm_tune_save(const char* path) {
+  FILE* f = fopen(path, "w");
+  if (!f) return;
+  std::lock_guard<std::mutex> lk(tune_mu());
+  for (const auto& kv : tune_cache()) {
+    const GemmKey& k = kv.first;
+    fprintf(f, "%d %d %d %d %d %d %d %d %d %d %d %d %d %d %d\n", k.rows_out, k.w_out, k.B, k.N, k.cin, k.c0, k.taps, k.stride,
+            k.split_out, k.res, k.odt, k.st, kv.second.bn, kv.second.splits, kv.second.pair);
+  }
+  fclose(f);
+}
+
 // Time every legal (BN, split-K) configuration of this GEMM shape on its real buffers and cache the
 // fastest (called at plan time, outside graph capture; outputs are scratch at that point).
 void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {

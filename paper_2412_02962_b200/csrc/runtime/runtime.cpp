@@ -424,10 +424,15 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s);
 bool gemm_tc_supported(const GemmArgs& g);
 
 // Per-shape GEMM configuration search on the plan's own buffers (before any graph capture).
+void gemm_tune_load(const char* path);
+void gemm_tune_save(const char* path);
+
 pcpp_status plan_autotune(Plan& P) {
   if (!P.use_tc) return PCPP_OK;
   static const int env = getenv("PCPP_AUTOTUNE") ? atoi(getenv("PCPP_AUTOTUNE")) : 1;
   if (!env) return PCPP_OK;
+  static bool loaded = false;
+  if (!loaded && getenv("PCPP_TUNE_FILE")) { gemm_tune_load(getenv("PCPP_TUNE_FILE")); loaded = true; }
   const size_t es = dtype_size(P.dtype);
   const char* wm = reinterpret_cast<const char*>(P.wmat);
   for (const Op& op : P.ops) {
@@ -453,6 +458,7 @@ pcpp_status plan_autotune(Plan& P) {
     if (op.gn_fuse >= 0) { g.gn_part = reinterpret_cast<float*>(P.rm[0].arena + P.off_epart); g.gn_slots = &slots; }
     if (gemm_tc_supported(g)) gemm_tc_autotune(g, P.s0);
   }
+  if (getenv("PCPP_TUNE_SAVE")) gemm_tune_save(getenv("PCPP_TUNE_SAVE"));
   CK(cudaStreamSynchronize(P.s0));
   CK(cudaGetLastError());
   return PCPP_OK;
