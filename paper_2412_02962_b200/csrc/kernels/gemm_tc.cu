@@ -273,30 +273,41 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0;
+      // single-thread TMA producer: ring slot / phase and the (tap, channel chunk) walk are kept
+      // incrementally (no divisions in the k loop)
+      int st = 0;
+      uint32_t ph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int r0, b0, w0, n0, z;
         decode(u, r0, b0, w0, n0, z);
         const int s_begin = z * p.s_len, s_end = min(nsteps_all, s_begin + p.s_len);
-        for (int s = s_begin; s < s_end; ++s, ++it) {
-          const int st = it % Cfg::STAGES;
-          const uint32_t ph = (it / Cfg::STAGES) & 1;
+        int tap = s_begin / p.nkc, kc = s_begin - tap * p.nkc;
+        int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
+        const int wa = w0 * p.stride, ra = r0 * p.stride + p.pad;
+        for (int s = s_begin; s < s_end; ++s) {
           sm100::mbar_wait(&empty[st], ph ^ 1);
-          const int tap = s / p.nkc, kc = s - tap * p.nkc;
-          const int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
           sm100::mbar_arrive_expect_tx(&full[st], p.a_bytes + Cfg::B_BYTES);
           if (kc < p.nk0)
-            sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma0, &full[st], kc * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
+            sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma0, &full[st], kc * 64, wa + dw, b0, ra + dr);
           else
-            sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma1, &full[st], (kc - p.nk0) * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
+            sm100::tma_load_4d(sA + st * Cfg::A_BYTES, &p.ma1, &full[st], (kc - p.nk0) * 64, wa + dw, b0, ra + dr);
           sm100::tma_load_2d(sB + st * Cfg::B_BYTES, &p.mb, &full[st], s * 64, n0);
+          if (++kc == p.nkc) {
+            kc = 0;
+            if (p.taps == 9 && ++dw == 2) { dw = -1; ++dr; }
+          }
+          if (++st == Cfg::STAGES) { st = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
+      // single-thread MMA issuer: descriptors advance by constant offsets (address field = bytes >> 4)
       constexpr uint32_t idesc = sm100::idesc_bf16(128, BN, 0, 0);
-      int it = 0, tc = 0;
+      const uint64_t a_desc0 = sm100::sdesc_sw128(sm100::smem_u32(sA), 16, 1024);
+      const uint64_t b_desc0 = sm100::sdesc_sw128(sm100::smem_u32(sB), 16, 1024);
+      int st = 0, tc = 0;
+      uint32_t ph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++tc) {
         int r0, b0, w0, n0, z;
         decode(u, r0, b0, w0, n0, z);
@@ -305,20 +316,19 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
         sm100::mbar_wait(&tempty[a], ((tc >> 1) & 1) ^ 1);
         sm100::fence_after();
         const uint32_t d = tmem + a * BN;
-        for (int s = s_begin; s < s_end; ++s, ++it) {
-          const int st = it % Cfg::STAGES;
-          const uint32_t ph = (it / Cfg::STAGES) & 1;
+        uint32_t acc = 0;
+        for (int s = s_begin; s < s_end; ++s) {
           sm100::mbar_wait(&full[st], ph);
           sm100::fence_after();
-          const uint32_t a_base = sm100::smem_u32(sA + st * Cfg::A_BYTES);
-          const uint32_t b_base = sm100::smem_u32(sB + st * Cfg::B_BYTES);
+          const uint64_t ad = a_desc0 + (uint64_t)((st * Cfg::A_BYTES) >> 4);
+          const uint64_t bd = b_desc0 + (uint64_t)((st * Cfg::B_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = sm100::sdesc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bd = sm100::sdesc_sw128(b_base + k * 32, 16, 1024);
-            sm100::mma_bf16_ss(d, ad, bd, idesc, ((s - s_begin) | k) != 0);
+            sm100::mma_bf16_ss(d, ad + 2 * k, bd + 2 * k, idesc, acc);
+            acc = 1;
           }
           sm100::mma_commit(&empty[st]);
+          if (++st == Cfg::STAGES) { st = 0; ph ^= 1; }
         }
         sm100::mma_commit(&tfull[a]);
       }
@@ -510,31 +520,40 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0;
+      int st = 0;
+      uint32_t ph = 0;
       for (int u = cid; u < units; u += ncl) {
         int r0, b0, w0, n0, z;
         decode(u, r0, b0, w0, n0, z);
         const int s_begin = z * p.s_len, s_end = min(nsteps_all, s_begin + p.s_len);
-        for (int s = s_begin; s < s_end; ++s, ++it) {
-          const int st = it % Cfg::STAGES;
-          const uint32_t ph = (it / Cfg::STAGES) & 1;
+        int tap = s_begin / p.nkc, kc = s_begin - tap * p.nkc;
+        int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
+        const int wa = w0 * p.stride, ra = r0 * p.stride + p.pad;
+        const int nb = n0 + (int)rank * (BN / 2);
+        for (int s = s_begin; s < s_end; ++s) {
           sm100::mbar_wait_cluster(&empty[st], ph ^ 1);
-          const int tap = s / p.nkc, kc = s - tap * p.nkc;
-          const int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
           if (rank == 0) sm100::mbar_arrive_expect_tx(&full[st], 2 * (p.a_bytes + Cfg::B_BYTES));
           const uint32_t fb = sm100::leader_addr(&full[st]);
           if (kc < p.nk0)
-            sm100::tma_load_4d_2sm(sA + st * Cfg::A_BYTES, &p.ma0, fb, kc * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
+            sm100::tma_load_4d_2sm(sA + st * Cfg::A_BYTES, &p.ma0, fb, kc * 64, wa + dw, b0, ra + dr);
           else
-            sm100::tma_load_4d_2sm(sA + st * Cfg::A_BYTES, &p.ma1, fb, (kc - p.nk0) * 64, w0 * p.stride + dw, b0, r0 * p.stride + dr + p.pad);
-          sm100::tma_load_2d_2sm(sB + st * Cfg::B_BYTES, &p.mb, fb, s * 64, n0 + (int)rank * (BN / 2));
+            sm100::tma_load_4d_2sm(sA + st * Cfg::A_BYTES, &p.ma1, fb, (kc - p.nk0) * 64, wa + dw, b0, ra + dr);
+          sm100::tma_load_2d_2sm(sB + st * Cfg::B_BYTES, &p.mb, fb, s * 64, nb);
+          if (++kc == p.nkc) {
+            kc = 0;
+            if (p.taps == 9 && ++dw == 2) { dw = -1; ++dr; }
+          }
+          if (++st == Cfg::STAGES) { st = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       constexpr uint32_t idesc = sm100::idesc_bf16(256, BN, 0, 0);
-      int it = 0, tc = 0;
+      const uint64_t a_desc0 = sm100::sdesc_sw128(sm100::smem_u32(sA), 16, 1024);
+      const uint64_t b_desc0 = sm100::sdesc_sw128(sm100::smem_u32(sB), 16, 1024);
+      int st = 0, tc = 0;
+      uint32_t ph = 0;
       for (int u = cid; u < units; u += ncl, ++tc) {
         int r0, b0, w0, n0, z;
         decode(u, r0, b0, w0, n0, z);
@@ -543,18 +562,19 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
         sm100::mbar_wait_cluster(&tempty[a], ((tc >> 1) & 1) ^ 1);
         sm100::fence_after();
         const uint32_t d = tmem + a * BN;
-        for (int s = s_begin; s < s_end; ++s, ++it) {
-          const int st = it % Cfg::STAGES;
-          const uint32_t ph = (it / Cfg::STAGES) & 1;
+        uint32_t acc = 0;
+        for (int s = s_begin; s < s_end; ++s) {
           sm100::mbar_wait_cluster(&full[st], ph);
           sm100::fence_after();
-          const uint32_t a_base = sm100::smem_u32(sA + st * Cfg::A_BYTES);
-          const uint32_t b_base = sm100::smem_u32(sB + st * Cfg::B_BYTES);
+          const uint64_t ad = a_desc0 + (uint64_t)((st * Cfg::A_BYTES) >> 4);
+          const uint64_t bd = b_desc0 + (uint64_t)((st * Cfg::B_BYTES) >> 4);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            sm100::mma2_bf16_ss(d, sm100::sdesc_sw128(a_base + k * 32, 16, 1024), sm100::sdesc_sw128(b_base + k * 32, 16, 1024),
-                                idesc, ((s - s_begin) | k) != 0);
+          for (int k = 0; k < 4; ++k) {
+            sm100::mma2_bf16_ss(d, ad + 2 * k, bd + 2 * k, idesc, acc);
+            acc = 1;
+          }
           sm100::mma2_commit_mc(&empty[st], 0x3);
+          if (++st == Cfg::STAGES) { st = 0; ph ^= 1; }
         }
         sm100::mma2_commit_mc(&tfull[a], 0x3);
       }

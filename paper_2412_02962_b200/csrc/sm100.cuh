@@ -47,6 +47,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// try_wait without a suspend-time hint (the hardware's default window), looped
+__device__ __forceinline__ bool mbar_try_wait_nh(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_nh(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait_nh(a, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait_nh(a, parity)) {
+    if (clock64() - t0 > 20000000000LL) __trap();
+  }
+}
+
 // pure polling wait (mbarrier.test_wait, no suspend): for latency-critical single-thread issuers
 __device__ __forceinline__ bool mbar_test_wait(uint32_t a, uint32_t parity) {
   uint32_t ok;
