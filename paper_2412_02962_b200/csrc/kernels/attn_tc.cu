@@ -118,37 +118,40 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         const int qt = qt0 + g;
         sm100::tma_load_4d(smem + SM_Q + g * TILE, &p.mq, q_full, head * 64, (qt % p.nWt) * p.Wbox, b, (qt / p.nWt) * p.Rbox);
       }
+      int st = 0;
+      uint32_t ph = 0;
+      int s, r0, w0;
+      tile_coords(p, j0, s, r0, w0);            // then walked incrementally (sources, rows, columns)
       for (int jj = 0; jj < nt; ++jj) {
-        const int st = jj % KST;
-        sm100::mbar_wait(&kv_empty[st], ((jj / KST) & 1) ^ 1);
-        int s, r0, w0;
-        tile_coords(p, j0 + jj, s, r0, w0);
+        sm100::mbar_wait(&kv_empty[st], ph ^ 1);
         sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * p.box_bytes);
         sm100::tma_load_4d(smem + SM_K + st * TILE, &p.mkv[s], &kv_full[st], head * 64, w0, b, r0);
         sm100::tma_load_4d(smem + SM_V + st * TILE, &p.mkv[s], &kv_full[st], p.C + head * 64, w0, b, r0);
+        if ((w0 += p.Wbox) >= p.W) { w0 = 0; if ((r0 += p.Rbox) >= p.rows[s]) { r0 = 0; ++s; } }
+        if (++st == KST) { st = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t id_s = sm100::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t id_o = sm100::idesc_bf16(128, 64, 0, 1);
+      // descriptors advance by constant offsets (address field = bytes >> 4); ring slots incremental
+      const uint64_t q_desc = sm100::sdesc_sw128(sm100::smem_u32(smem + SM_Q), 16, 1024);
+      const uint64_t k_desc = sm100::sdesc_sw128(sm100::smem_u32(smem + SM_K), 16, 1024);
+      const uint64_t p_desc = sm100::sdesc_sw128(sm100::smem_u32(smem + SM_P), 16, 1024);
+      const uint64_t v_desc = sm100::sdesc_sw128(sm100::smem_u32(smem + SM_V), 16384, 1024);
       sm100::mbar_wait(q_full, 0);
-      auto issue_s = [&](int g, int j) {
-        const uint32_t q_base = sm100::smem_u32(smem + SM_Q + g * TILE);
-        const uint32_t k_base = sm100::smem_u32(smem + SM_K + (j % KST) * TILE);   // j: local tile index
+      auto issue_s = [&](int g, int st) {
+        const uint64_t qd = q_desc + (uint64_t)((g * TILE) >> 4), kd = k_desc + (uint64_t)((st * TILE) >> 4);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          sm100::mma_bf16_ss(tmem + g * 128, sm100::sdesc_sw128(q_base + k * 32, 16, 1024),
-                             sm100::sdesc_sw128(k_base + k * 32, 16, 1024), id_s, k != 0);
+        for (int k = 0; k < 4; ++k) sm100::mma_bf16_ss(tmem + g * 128, qd + 2 * k, kd + 2 * k, id_s, k != 0);
         sm100::mma_commit(&s_full[g]);
       };
-      auto issue_o = [&](int g, int j) {
-        const uint32_t p_base = sm100::smem_u32(smem + SM_P + g * 2 * TILE);
-        const uint32_t v_base = sm100::smem_u32(smem + SM_V + (j % KST) * TILE);
+      auto issue_o = [&](int g, int st, bool first) {
+        const uint64_t pd = p_desc + (uint64_t)((g * 2 * TILE) >> 4), vd = v_desc + (uint64_t)((st * TILE) >> 4);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          sm100::mma_bf16_ss(tmem + 256 + g * 64, sm100::sdesc_sw128(p_base + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
-                             sm100::sdesc_sw128(v_base + k * 2048, 16384, 1024), id_o, (j | k) != 0);
+          sm100::mma_bf16_ss(tmem + 256 + g * 64, pd + (k >> 2) * 1024 + (k & 3) * 2, vd + k * 128, id_o, (!first || k != 0) ? 1u : 0u);
         sm100::mma_commit(&o_full[g]);
       };
       if (nt > 0) {
@@ -156,19 +159,23 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         sm100::fence_after();
         for (int g = 0; g < nwg; ++g) issue_s(g, 0);
       }
+      int st = 0, st1 = KST > 1 ? 1 : 0;        // ring slots of tiles j and j + 1
+      uint32_t ph1 = KST > 1 ? 0 : 1;           // phase of kv_full for tile j + 1
       for (int j = 0; j < nt; ++j) {
         for (int g = 0; g < nwg; ++g) {
           if (j + 1 < nt) {                          // S_g(j+1) as soon as softmax g is done reading S_g(j)
             sm100::mbar_wait(&s_free[g], j & 1);
-            if (g == 0) sm100::mbar_wait(&kv_full[(j + 1) % KST], ((j + 1) / KST) & 1);
+            if (g == 0) sm100::mbar_wait(&kv_full[st1], ph1);
             sm100::fence_after();
-            issue_s(g, j + 1);
+            issue_s(g, st1);
           }
           sm100::mbar_wait(&p_full[g], j & 1);      // P_g(j) written
           sm100::fence_after();
-          issue_o(g, j);
-          if (g == nwg - 1) sm100::mma_commit(&kv_empty[j % KST]);   // K_j, V_j free once both O MMAs finish
+          issue_o(g, st, j == 0);
+          if (g == nwg - 1) sm100::mma_commit(&kv_empty[st]);   // K_j, V_j free once both O MMAs finish
         }
+        st = st1;
+        if (++st1 == KST) { st1 = 0; ph1 ^= 1; }
       }
     }
   } else {
