@@ -48,6 +48,12 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ void tile_coords(const TcAttnParams& p, int j, int& s, int& r0, int& w0) {
   // enumerate sources in order, then row tiles, then column tiles
   s = 0;
@@ -91,8 +97,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
     sm100::mbar_init(q_full, 1);
     for (int i = 0; i < KST; ++i) { sm100::mbar_init(&kv_full[i], 1); sm100::mbar_init(&kv_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
-      sm100::mbar_init(&s_full[i], 1); sm100::mbar_init(&p_full[i], 128); sm100::mbar_init(&o_full[i], 1);
-      sm100::mbar_init(&s_free[i], 128);
+      sm100::mbar_init(&s_full[i], 1); sm100::mbar_init(&p_full[i], 4); sm100::mbar_init(&o_full[i], 1);
+      sm100::mbar_init(&s_free[i], 4);
     }
     sm100::fence_barrier_init();
   }
@@ -190,9 +196,10 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
       const float sl2 = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
       float m = -INFINITY, l = 0.f;
       uint8_t* P = smem + SM_P + g * 2 * TILE;
+      int s, r0, w0;
+      tile_coords(p, j0, s, r0, w0);            // then walked incrementally, like the producer
       for (int j = 0; j < nt; ++j) {
-        int s, r0, w0;
-        tile_coords(p, j0 + j, s, r0, w0);
+        if (j > 0 && (w0 += p.Wbox) >= p.W) { w0 = 0; if ((r0 += p.Rbox) >= p.rows[s]) { r0 = 0; ++s; } }
         const int nvr = min(p.Rbox, p.rows[s] - r0);
         const int nvw = min(p.Wbox, p.W - w0);
         const int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;   // valid keys form a prefix
@@ -213,9 +220,9 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         }
         float mx = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 64; i += 2) mx = fmaxf(mx, fmaxf(hi[i], hi[i + 1]));
+        for (int i = 0; i < 64; i += 2) mx = max3(mx, hi[i], hi[i + 1]);
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(lo[i], lo[i + 1]));
+        for (int i = 0; i < 32; i += 2) mx = max3(mx, lo[i], lo[i + 1]);
         sm100::tmem_ld32(t_s + 32, reinterpret_cast<uint32_t*>(lo));
         sm100::tmem_wait_ld();
         if (nvalid < 128) {
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
           for (int i = 0; i < 32; ++i) if (32 + i >= nvalid) lo[i] = -INFINITY;
         }
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(lo[i], lo[i + 1]));
+        for (int i = 0; i < 32; i += 2) mx = max3(mx, lo[i], lo[i + 1]);
         mx *= sl2;
         const bool raise = mx > m + 8.0f;
         const float m_new = raise ? mx : m;
@@ -258,7 +265,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         sm100::tmem_ld32(t_s + 0, reinterpret_cast<uint32_t*>(lo));
         sm100::tmem_wait_ld();
         sm100::fence_before();
-        sm100::mbar_arrive(&s_free[g]);                                        // S(j) no longer read
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&s_free[g]);     // S(j) no longer read (one arrival per warp)
         if (nvalid < 128) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) if (i >= nvalid) lo[i] = -INFINITY;
@@ -271,7 +279,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1) attn_tc_kernel(const __grid_c
         m = m_new;
         sm100::fence_proxy_async_smem();
         sm100::fence_before();
-        sm100::mbar_arrive(&p_full[g]);
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&p_full[g]);     // one arrival per warp
       }
       if (nt > 0) {
         sm100::mbar_wait(&o_full[g], (nt - 1) & 1);
