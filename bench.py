@@ -258,16 +258,33 @@ def main():
             prof[name] = plan.pcpp_profile(lat, mask, 0, 5)
     peaks = measured_peaks()
     roof = None
+    roof_attn = None
     if prof:
         g = prof["conv_gemm"]
         peak = peaks.get("bf16_tflops", 1590.0)
         ach = g["flops"] / (g["ms"] * 1e-3) / 1e12
+        traffic, tsrc = None, None
+        tfile = os.path.join(ROOT, "profiles", "r1_gemm_traffic_step.json")
+        if os.path.exists(tfile) and args.res == 128 and world == 1 and args.scheme == "pcpp":
+            tj = json.load(open(tfile))
+            traffic, tsrc = tj["gemm_dram_bytes_per_launch"], tj["source"]
         roof = {"kernel": "gemm_tc_kernel (implicit-GEMM conv3x3 / 1x1, tcgen05) + its SIMT fallbacks",
                 "bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(ach / peak, 4), "traffic": None,
+                "frac": round(ach / peak, 4), "traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write)",
+                "traffic_source": tsrc,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; kernel timed alone)" if peaks else "fallback",
                 "per_launch_flops": g["flops"] / max(g["launches"], 1),
                 "avg_launch_ms": g["ms"] / max(g["launches"], 1)}
+        # second kernel family: the attention is bound by exp2 on the MUFU (16/clk/SM measured,
+        # tools/ubench/mufu.cu -> 4.63e12/s at 1965 MHz), one exp2 per score = flops / (4 * 64)
+        a = prof["attention"]
+        if a["launches"]:
+            ex = a["flops"] / 256.0 / (a["ms"] * 1e-3)
+            roof_attn = {"kernel": "attn_tc_kernel (partially conditioned flash attention, tcgen05)", "bound": "alu",
+                         "what": "exp2 on the MUFU (d = 64: 2 exp-bound clk per 1 tensor clk)",
+                         "achieved": round(ex / 1e12, 3), "peak": 4.63, "unit": "Texp2/s",
+                         "frac": round(ex / 4.63e12, 4), "tensor_tflops": round(a["flops"] / (a["ms"] * 1e-3) / 1e12, 1),
+                         "peak_source": "measured 16 ex2/clk/SM x 148 SMs x 1.965 GHz (profiles/r1_ubench.txt)"}
 
     # end to end through the public API: pcpp_sample with pinned host buffers (x_T in, x_0 out)
     e2e = None
@@ -316,7 +333,7 @@ def main():
             "achieved_tflops_step": round(info["step_flops_rank_max"] / (ms * 1e-3) / 1e12, 1),
             "gpu_launches": info["n_kernels_per_step"] * args.steps,
             "clocks": clk.summary(),
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "roofline": roof, "roofline_attention": roof_attn, "cpu_baseline": cpu,
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in prof.items()},
             "context": "paper: 2.36-8.02x speed-up on 4-8 A100-40GB, SDXL fp16 (P:5); not comparable hardware",
         }
