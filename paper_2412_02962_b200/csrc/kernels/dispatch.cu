@@ -17,9 +17,12 @@ bool gemm_tc_supported(const GemmArgs& g);
 bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
 void gemm_tc_init();
 
+bool launch_conv_in(const GemmArgs& g, cudaStream_t s);
+
 void launch_gemm_auto(const GemmArgs& g, bool allow_tc, cudaStream_t s) {
   if (g.gn_slots) *g.gn_slots = 0;
   if (allow_tc && gemm_tc_supported(g) && launch_gemm_tc(g, s)) return;
+  if (allow_tc && launch_conv_in(g, s)) return;          // Cin = 4 latent conv (bf16 mode)
   launch_gemm_simt(g, s);
 }
 bool attn_tc_supported(const AttnArgs& a);

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // SIMT implicit-GEMM conv3x3 / 1x1 (fp32 accumulate).  Used for:
 //  * every contraction in fp32 mode (parity mode, rel-L2 <= 1e-5; no fp32 tensor-core kind exists),
 //  * conv_in (Cin = 4) in both modes, and as the bf16 fallback for shapes the tcgen05 path rejects.
@@ -165,7 +166,105 @@ __global__ void __launch_bounds__(256) conv_out_kernel(const ActView in, const f
   }
 }
 
+// conv_in (Cin = 4, fp32 latent input, bf16 output): thread = output channel (its 36 weights and
+// bias in registers), the CTA walks 32 consecutive tokens of one row; each token's 3x3x4 input patch
+// is 9 warp-uniform 16-byte loads (L1 broadcast), stores are 2-byte per lane = contiguous per warp.
+__global__ void __launch_bounds__(320) conv_in_kernel(const ActView in, const float* __restrict__ w,
+                                                      const float* __restrict__ bias, const ActView out, int N) {
+  pdl_trigger();
+  const int n = threadIdx.x;
+  float wr[36];
+  float bi = 0.f;
+  if (n < N) {
+#pragma unroll
+    for (int i = 0; i < 36; ++i) wr[i] = w[n * 36 + i];
+    bi = bias ? bias[n] : 0.f;
+  }
+  pdl_wait();
+  if (n >= N) return;
+  const int nwt = (out.W + 31) / 32;
+  const int wt = blockIdx.x % nwt, rb = blockIdx.x / nwt;
+  const int b = rb % out.B, r = rb / out.B;
+  const float4* x = reinterpret_cast<const float4*>(in.base);   // [rows (+halo)][B][W] x 4 channels
+  bf16* y = reinterpret_cast<bf16*>(out.base);
+  for (int wo = wt * 32; wo < min(out.W, wt * 32 + 32); ++wo) {
+    float acc = bi;
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+      const int ri = r + tap / 3 - 1, wi = wo + tap % 3 - 1;
+      if (wi < 0 || wi >= in.W) continue;
+      const float4 v = __ldg(x + ((long long)ri * in.B + b) * in.W + wi);
+      acc = fmaf(v.x, wr[tap * 4], acc); acc = fmaf(v.y, wr[tap * 4 + 1], acc);
+      acc = fmaf(v.z, wr[tap * 4 + 2], acc); acc = fmaf(v.w, wr[tap * 4 + 3], acc);
+    }
+    y[(((long long)r * out.B + b) * out.W + wo) * out.C + n] = __float2bfloat16_rn(acc);
+  }
+}
+
+bool launch_conv_in(const GemmArgs& g, cudaStream_t s) {
+  if (!(g.taps == 9 && g.stride == 1 && g.cin == 4 && !g.a1.base && g.a0.dtype == DT_F32 && g.a0.C == 4 &&
+        g.wdtype == DT_F32 && g.out.dtype == DT_BF16 && !g.out2.base && !g.res.base && !g.temb && g.N <= 320 &&
+        g.out.C == g.N))
+    return false;
+  const int nwt = (g.w_out + 31) / 32;
+  launch_pdl(conv_in_kernel, dim3((unsigned)(g.rows_out * g.B * nwt)), dim3(((g.N + 31) / 32) * 32), 0, s, g.a0,
+             reinterpret_cast<const float*>(g.w), g.bias, g.out, g.N);
+  return true;
+}
+
+// conv_out for bf16 activations: lane = output token (128 consecutive tokens of one row per CTA),
+// the 9 x C x 4 fp32 weights staged once per CTA in shared memory as [tap * C + c][4] so one
+// broadcast 16-byte read feeds the 4 output channels; activations read as 16-byte channel vectors.
+__global__ void __launch_bounds__(128) conv_out_bf16_kernel(const ActView in, const float* __restrict__ w,
+                                                            const float* __restrict__ bias, const ActView out) {
+  pdl_trigger();
+  extern __shared__ float4 wsm[];                 // [9 * C] x {o0, o1, o2, o3}
+  const int C = in.C, K = 9 * C;
+  for (int i = threadIdx.x; i < K; i += blockDim.x)
+    wsm[i] = make_float4(w[i], w[K + i], w[2 * K + i], w[3 * K + i]);
+  __syncthreads();
+  pdl_wait();
+  const int nwt = (out.W + 127) / 128;
+  const int wt = blockIdx.x % nwt;
+  const int rb = blockIdx.x / nwt;                 // r * B + b
+  const int b = rb % out.B, r = rb / out.B;
+  const int wo = wt * 128 + threadIdx.x;
+  if (wo >= out.W) return;
+  const bf16* x = reinterpret_cast<const bf16*>(in.base);
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 1
+  for (int tap = 0; tap < 9; ++tap) {
+    const int ri = r + tap / 3 - 1, wi = wo + tap % 3 - 1;
+    if (wi < 0 || wi >= in.W) continue;                // zero padding left / right (halo rows exist)
+    const uint4* px = reinterpret_cast<const uint4*>(x + (((long long)ri * in.B + b) * in.W + wi) * C);
+    const float4* pw = wsm + tap * C;
+#pragma unroll 2
+    for (int c8 = 0; c8 < C / 8; ++c8) {
+      const uint4 u = __ldg(px + c8);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        const float4 w0 = pw[c8 * 8 + 2 * e], w1 = pw[c8 * 8 + 2 * e + 1];
+        a0 = fmaf(f.x, w0.x, a0); a1 = fmaf(f.x, w0.y, a1); a2 = fmaf(f.x, w0.z, a2); a3 = fmaf(f.x, w0.w, a3);
+        a0 = fmaf(f.y, w1.x, a0); a1 = fmaf(f.y, w1.y, a1); a2 = fmaf(f.y, w1.z, a2); a3 = fmaf(f.y, w1.w, a3);
+      }
+    }
+  }
+  float4* po = reinterpret_cast<float4*>(reinterpret_cast<float*>(out.base) + (((long long)r * out.B + b) * out.W + wo) * 4);
+  *po = make_float4(a0 + bias[0], a1 + bias[1], a2 + bias[2], a3 + bias[3]);
+}
+
 void launch_conv_out(const ActView& in, const float* w, const float* bias, const ActView& out, cudaStream_t s) {
+  static const int v2 = getenv("PCPP_CONV_OUT_V2") ? atoi(getenv("PCPP_CONV_OUT_V2")) : 0;   // measured slower
+  if (v2 && in.dtype == DT_BF16 && in.C % 8 == 0 && out.C == 4 && (size_t)in.C * 9 * 16 <= 160 * 1024) {
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(conv_out_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); attr = true; }
+    const int nwt = (out.W + 127) / 128;
+    launch_pdl(conv_out_bf16_kernel, dim3((unsigned)(out.rows * out.B * nwt)), dim3(128), (size_t)in.C * 9 * 16, s, in, w,
+               bias, out);
+    return;
+  }
   const long long M = (long long)out.rows * out.B * out.W;
   dim3 grid((unsigned)((M + 7) / 8));
   if (in.dtype == DT_F32) launch_pdl(conv_out_kernel<float>, dim3(grid), dim3(256), 0, s, in, w, bias, out);
