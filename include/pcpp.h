@@ -72,7 +72,13 @@ typedef struct {
   int comm_backend;           /* PCPP_COMM_NCCL | PCPP_COMM_LOOPBACK */
   int kernels;                /* PCPP_KERNELS_AUTO | PCPP_KERNELS_SIMT */
   int use_graphs;             /* 1: replay per-step CUDA graphs ("CUDA Graph"); 0: eager */
+  int scheduler;              /* PCPP_SCHED_DDIM (0, default) | PCPP_SCHED_DPMPP2M (1): DPM-Solver++(2M)
+                                 on the same timestep ladder (north star "DDIM/DPM-solver"; DESIGN.md
+                                 reading D23).  Elementwise and patch-local: no exchange. */
 } pcpp_config;
+
+#define PCPP_SCHED_DDIM 0
+#define PCPP_SCHED_DPMPP2M 1
 
 #define PCPP_MAX_LAYERS 128
 

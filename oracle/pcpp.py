@@ -5,7 +5,8 @@ Follows, in the paper's order:
   * the first w steps are synchronous (§3.2 "initial warm-up steps where
     we perform synchronous AllGather"; w = 4 in Table 2, P:173);
   * later steps read neighbour data stale from step t+1 (P:89 §3.2; Eq. 1);
-  * per rank: CFG (Eq. 2, P:58) and the DDIM update (P:134) on its own patch;
+  * per rank: CFG (Eq. 2) and the DDIM update -- or DPM-Solver++(2M),
+    reading D23 -- on its own patch (the scheduler is elementwise: patch-local);
   * scheme 'fullmap' is the DistriFusion baseline (§3.2): every
     attention layer reads all other ranks' stale K/V;
   * scheme 'sync' runs every step synchronously (domain parallelism).
@@ -20,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import model as M
-from .schedule import cfg_combine, ddim_step, ddim_timesteps
+from .schedule import cfg_combine, ddim_step, ddim_timesteps, dpmpp_2m_step
 
 
 @dataclass
@@ -34,6 +35,7 @@ class Config:
     steps: int = 4
     guidance: float = 5.0
     scheme: str = "pcpp"          # 'pcpp' | 'fullmap' | 'sync'
+    scheduler: str = "ddim"       # 'ddim' | 'dpmpp2m' (north star "DPM-solver", reading D23)
     extras: dict = field(default_factory=dict)
 
 
@@ -68,7 +70,14 @@ def sample(cfg: Config, blob: np.ndarray, x_T: np.ndarray, cond: np.ndarray,
         emb = M.timestep_embedding(P, cfg.model, taus[k], cond)
         eps = M.unet(ctx, P, cfg.model, patches, emb)
         eps_hat = [cfg_combine(e[0], e[1], cfg.guidance) for e in eps]   # b=0 uncond, b=1 cond
-        patches = [ddim_step(x, e, cfg.steps, k) for x, e in zip(patches, eps_hat)]
+        if cfg.scheduler == "dpmpp2m":
+            if k == 0:
+                x0_hist = [None] * n
+            res = [dpmpp_2m_step(x, e, cfg.steps, k, x0p) for x, e, x0p in zip(patches, eps_hat, x0_hist)]
+            patches = [r[0] for r in res]
+            x0_hist = [r[1] for r in res]
+        else:
+            patches = [ddim_step(x, e, cfg.steps, k) for x, e in zip(patches, eps_hat)]
         prev = ctx.nxt
         if record:
             out["xs"].append(np.concatenate(patches, axis=0))

@@ -13,10 +13,16 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 * rows(p, h): Eq. 1 takes "p h" rows of a neighbour; reading D1:
   floor(p h + 1e-9), at least one row when p > 0, at most h.
 
+* DPM-Solver++(2M) (north star "DDIM/DPM-solver"; reading D23): data-prediction multistep on
+  the same timestep ladder; first order at k = 0 (and at the last step when S < 15).
+
 Pins (tests/test_oracle_schedule.py): alpha_bar = prod(1 - beta); DDIM step on
 an exact x_tau = sqrt(ab) x0 + sqrt(1-ab) eps returns sqrt(ab') x0 +
 sqrt(1-ab') eps; CFG identities s=1 -> eps_c, eps_c = eps_u -> eps_u; the
-printed p values of Fig. 4 give integer row counts.
+printed p values of Fig. 4 give integer row counts; DPM-Solver++ first
+order == DDIM; on an exact trajectory every 2M step is exact; against the closed-form
+solution of the data-prediction ODE for x0 linear in lambda the 2M sampler converges at
+order 2 (the first-order sampler at order 1).
 """
 from __future__ import annotations
 
@@ -80,6 +86,54 @@ def ddim_step(x: np.ndarray, eps_hat: np.ndarray, num_steps: int, k: int) -> np.
     sa, s1a, sp, s1p = ddim_coeffs(num_steps, k)
     x0 = (x - s1a * eps_hat) / sa
     return sp * x0 + s1p * eps_hat
+
+
+def dpmpp_2m_second_order(num_steps: int, k: int) -> bool:
+    """Reading D23: DPM-Solver++(2M) takes a first-order step at k = 0 (no history) and, for
+    S < 15, at the final step (diffusers' lower_order_final); second order otherwise."""
+    if k == 0:
+        return False
+    if num_steps < 15 and k == num_steps - 1:
+        return False
+    return True
+
+
+def _lam(ab: float) -> float:
+    """lambda_t = log(alpha_t / sigma_t), alpha_t = sqrt(ab), sigma_t = sqrt(1 - ab)."""
+    return 0.5 * math.log(ab) - 0.5 * math.log(1.0 - ab)
+
+
+def dpmpp_2m_step(x: np.ndarray, eps_hat: np.ndarray, num_steps: int, k: int, x0_prev):
+    """DPM-Solver++(2M) (Lu et al. 2022, data-prediction multistep, Algorithm 2) on the DDIM
+    timestep ladder of reading D2 (north star: "the DDIM/DPM-solver scheduler update").
+
+      x0_k = (x - sigma_k eps) / alpha_k,   h = lambda' - lambda_k
+      first order:  x' = (sigma'/sigma_k) x - alpha' (e^{-h} - 1) x0_k        (== DDIM)
+      second order: r = h_prev / h,  D = (1 + 1/(2r)) x0_k - (1/(2r)) x0_{k-1}
+                    x' = (sigma'/sigma_k) x - alpha' (e^{-h} - 1) D
+
+    Returns (x', x0_k); x0_k is the history the next step needs.
+    """
+    ab = alpha_bars()
+    taus = ddim_timesteps(num_steps)
+    step = NUM_TRAIN_TIMESTEPS // num_steps
+
+    def abar(t):
+        return ab[t] if t >= 0 else ab[0]
+
+    a_t = abar(taus[k])
+    a_p = abar(taus[k] - step)
+    alpha_t, sigma_t = math.sqrt(a_t), math.sqrt(1.0 - a_t)
+    alpha_p, sigma_p = math.sqrt(a_p), math.sqrt(1.0 - a_p)
+    h = _lam(a_p) - _lam(a_t)
+    x0 = (x - sigma_t * eps_hat) / alpha_t
+    if dpmpp_2m_second_order(num_steps, k):
+        h_prev = _lam(a_t) - _lam(abar(taus[k - 1]))
+        r = h_prev / h
+        D = (1.0 + 1.0 / (2.0 * r)) * x0 - (1.0 / (2.0 * r)) * x0_prev
+    else:
+        D = x0
+    return (sigma_p / sigma_t) * x - alpha_p * math.expm1(-h) * D, x0
 
 
 def ddpm_mean(x: np.ndarray, eps_hat: np.ndarray, t: int) -> np.ndarray:

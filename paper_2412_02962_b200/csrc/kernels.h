@@ -93,6 +93,10 @@ void launch_upsample2(const ActView& in, const ActView& out, cudaStream_t s);
 // Eq. 2 + DDIM: eps [h][2][W][4] fp32; latent [h][W][4] fp32 in place; coef[k*4 + {sa,s1a,sp,s1p}]
 void launch_cfg_ddim(const float* eps, float* latent, int h, int W, float s_cfg,
                      const double* coef, const int* k_dev, cudaStream_t s);
+// Eq. 2 + DPM-Solver++(2M) (reading D23): x0 = (x - sigma eps) / alpha; x <- A x + Bc (w0 x0 + w1 x0_hist);
+// x0_hist <- x0.  coef[k*6 + {1/alpha, sigma, A, Bc, w0, w1}]
+void launch_cfg_dpmpp(const float* eps, float* latent, float* x0_hist, int h, int W, float s_cfg,
+                      const double* coef, const int* k_dev, cudaStream_t s);
 void launch_step_end(int* k_dev, cudaStream_t s);
 
 // timestep embedding: emb[b][T] for tau = taus[*k_dev]; then tproj[b][j] for all ResBlocks

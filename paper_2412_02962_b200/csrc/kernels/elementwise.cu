@@ -82,6 +82,44 @@ void launch_cfg_ddim(const float* eps, float* latent, int h, int W, float s_cfg,
                                          h, W, s_cfg, coef, k_dev);
 }
 
+// DPM-Solver++(2M), multistep data prediction (north star "DDIM/DPM-solver"; reading D23)
+__global__ void cfg_dpmpp_kernel(const float4* __restrict__ eps, float4* __restrict__ lat, float4* __restrict__ x0h,
+                                 int h, int W, float s_cfg, const double* __restrict__ coef, const int* __restrict__ k_dev) {
+  pdl_trigger();
+  pdl_wait();
+  const int k = *k_dev;
+  const float inv_a = (float)coef[6 * k + 0], sig = (float)coef[6 * k + 1];
+  const float A = (float)coef[6 * k + 2], Bc = (float)coef[6 * k + 3];
+  const float w0 = (float)coef[6 * k + 4], w1 = (float)coef[6 * k + 5];
+  const long long n = (long long)h * W;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / W, w = i % W;
+    const float4 eu = eps[(r * 2 + 0) * W + w], ec = eps[(r * 2 + 1) * W + w];
+    float4 x = lat[i];
+    float4 xp = x0h[i];
+    const float e[4] = {eu.x + s_cfg * (ec.x - eu.x), eu.y + s_cfg * (ec.y - eu.y),
+                        eu.z + s_cfg * (ec.z - eu.z), eu.w + s_cfg * (ec.w - eu.w)};
+    float* xv = &x.x;
+    float* pv = &xp.x;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float x0 = (xv[c] - sig * e[c]) * inv_a;
+      const float D = w1 != 0.f ? fmaf(w0, x0, w1 * pv[c]) : x0;   // first-order steps never read the history
+      xv[c] = fmaf(A, xv[c], Bc * D);
+      pv[c] = x0;
+    }
+    lat[i] = x;
+    x0h[i] = xp;
+  }
+}
+void launch_cfg_dpmpp(const float* eps, float* latent, float* x0_hist, int h, int W, float s_cfg,
+                      const double* coef, const int* k_dev, cudaStream_t s) {
+  const long long n = (long long)h * W;
+  int blocks = (int)((n + 255) / 256); if (blocks > 1184) blocks = 1184;
+  launch_pdl(cfg_dpmpp_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const float4*>(eps),
+             reinterpret_cast<float4*>(latent), reinterpret_cast<float4*>(x0_hist), h, W, s_cfg, coef, k_dev);
+}
+
 __global__ void step_end_kernel(int* k_dev) {
   pdl_trigger();
   pdl_wait(); *k_dev += 1; }

@@ -120,6 +120,8 @@ pcpp_status plan_allocate(Plan& P) {
   P.emb = (float*)galloc(2 * P.T * 4); P.hid = (float*)galloc(P.T * 4);
   P.tproj = (float*)galloc((size_t)2 * P.J * 4); P.cond = (float*)galloc(P.T * 4);
   P.taus = (int*)galloc(P.S * 4); P.coef = (double*)galloc(P.S * 4 * 8); P.k_dev = (int*)galloc(16);
+  P.coef_dpm = (double*)galloc(P.S * 6 * 8);
+  if (P.cfg.scheduler == PCPP_SCHED_DPMPP2M) P.x0_hist = (float*)galloc((size_t)P.nr * (P.H / P.n) * P.W * 4 * 4);
   if (P.dtype == DT_BF16) {       // split-K workspace: up to 8 fp32 partial copies of the largest GEMM output
     size_t mx = 0;
     for (const Op& o : P.ops)
@@ -152,6 +154,28 @@ pcpp_status plan_allocate(Plan& P) {
     coef[4 * k + 0] = std::sqrt(at); coef[4 * k + 1] = std::sqrt(1.0 - at);
     coef[4 * k + 2] = std::sqrt(ap); coef[4 * k + 3] = std::sqrt(1.0 - ap);
   }
+  // DPM-Solver++(2M) on the same ladder (reading D23): lambda = log(alpha / sigma); first order at
+  // k = 0 and, for S < 15, at the final step; x' = A x + Bc (w0 x0_k + w1 x0_{k-1})
+  std::vector<double> cd(6 * P.S);
+  auto lam = [](double a) { return 0.5 * std::log(a) - 0.5 * std::log(1.0 - a); };
+  for (int k = 0; k < P.S; ++k) {
+    const int tau = (P.S - 1 - k) * ratio + 1;
+    const int prev = tau - ratio;
+    const double at = ab[tau], ap = prev >= 0 ? ab[prev] : ab[0];
+    const double h = lam(ap) - lam(at);
+    const bool second = k > 0 && !(P.S < 15 && k == P.S - 1);
+    double w0 = 1.0, w1 = 0.0;
+    if (second) {
+      const double aq = ab[tau + ratio];                      // the previous ladder point
+      const double r = (lam(at) - lam(aq)) / h;
+      w0 = 1.0 + 1.0 / (2.0 * r); w1 = -1.0 / (2.0 * r);
+    }
+    cd[6 * k + 0] = 1.0 / std::sqrt(at); cd[6 * k + 1] = std::sqrt(1.0 - at);
+    cd[6 * k + 2] = std::sqrt(1.0 - ap) / std::sqrt(1.0 - at);
+    cd[6 * k + 3] = -std::sqrt(ap) * std::expm1(-h);
+    cd[6 * k + 4] = w0; cd[6 * k + 5] = w1;
+  }
+  CK(cudaMemcpy(P.coef_dpm, cd.data(), P.S * 6 * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(P.taus, taus.data(), P.S * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(P.coef, coef.data(), P.S * 4 * 8, cudaMemcpyHostToDevice));
   return PCPP_OK;
@@ -620,8 +644,12 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
         const int h = P.H / n;
         for (int vr = 0; vr < nr; ++vr) {
           float* lat = latent + (P.loopback ? (size_t)vr * h * P.W * 4 : 0);
-          launch_cfg_ddim(reinterpret_cast<const float*>(view(P, vr, op.in0, par).base), lat, h, P.W,
-                          P.cfg.guidance_scale, P.coef, P.k_dev, s);
+          if (P.cfg.scheduler == PCPP_SCHED_DPMPP2M)
+            launch_cfg_dpmpp(reinterpret_cast<const float*>(view(P, vr, op.in0, par).base), lat,
+                             P.x0_hist + (size_t)vr * h * P.W * 4, h, P.W, P.cfg.guidance_scale, P.coef_dpm, P.k_dev, s);
+          else
+            launch_cfg_ddim(reinterpret_cast<const float*>(view(P, vr, op.in0, par).base), lat, h, P.W,
+                            P.cfg.guidance_scale, P.coef, P.k_dev, s);
         }
         P.launches_per_step += nr;
         break;

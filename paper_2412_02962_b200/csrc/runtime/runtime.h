@@ -107,6 +107,8 @@ struct Plan {
   void* wmat = nullptr;  float* wf32 = nullptr;
   float* emb = nullptr; float* hid = nullptr; float* tproj = nullptr; float* cond = nullptr;
   int* taus = nullptr; double* coef = nullptr; int* k_dev = nullptr;
+  double* coef_dpm = nullptr;   // DPM-Solver++(2M): [S][6] {1/alpha, sigma, sigma'/sigma, -alpha'(e^-h - 1), w0, w1}
+  float* x0_hist = nullptr;     // DPM-Solver++(2M) data-prediction history, [nr][h][W][4] fp32
   float* ws = nullptr; size_t ws_elems = 0;   // split-K workspace
   std::vector<cudaEvent_t> op_ev; bool op_ev_on = false;   // per-op timing (PCPP_OP_TIMING, pcpp_profile)
   std::vector<void*> gallocs;

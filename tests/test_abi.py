@@ -93,3 +93,14 @@ def test_validation_channels_and_nccl_world():
     cfg = pcpp.make_config(model="sdxl", backend="nccl", world=4)
     with pytest.raises(pcpp.PcppError):
         pcpp.pcpp_plan_info(128, 128, 4, 2, 0.5, 1, cfg)
+
+
+def test_scheduler_validation():
+    """An unknown scheduler id is rejected before any allocation (PCPP_ERR_INVALID)."""
+    from paper_2412_02962_b200 import pcpp
+    cfg = pcpp.make_config(model="tiny", num_steps=4)
+    cfg.scheduler = 7
+    info = None
+    with pytest.raises(pcpp.PcppError):
+        info = pcpp.pcpp_plan_info(32, 32, 4, 2, 0.25, 1, cfg)
+    assert info is None

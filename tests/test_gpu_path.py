@@ -27,16 +27,16 @@ def weights(model, precision):
 
 
 @functools.lru_cache(maxsize=None)
-def oracle_run(model, H, n, p, w, S, precision, scheme, max_steps):
-    cfg = OP.Config(model=model, H=H, W=H, n=n, p=p, warmup=w, steps=S, scheme=scheme)
+def oracle_run(model, H, n, p, w, S, precision, scheme, max_steps, scheduler="ddim"):
+    cfg = OP.Config(model=model, H=H, W=H, n=n, p=p, warmup=w, steps=S, scheme=scheme, scheduler=scheduler)
     out = OP.sample(cfg, weights(model, precision), _data.latent(H, H), _data.cond(model), max_steps=max_steps)
     return out["xs"]
 
 
-def lib_run(model, H, n, p, w, S, precision, scheme, max_steps, kernels="auto", graphs=True):
+def lib_run(model, H, n, p, w, S, precision, scheme, max_steps, kernels="auto", graphs=True, scheduler="ddim"):
     import torch
     cfg = pcpp.make_config(model=model, num_steps=S, precision=precision, scheme=scheme, kernels=kernels,
-                           graphs=graphs)
+                           graphs=graphs, scheduler=scheduler)
     plan = pcpp.Plan(H, H, 4, n, p, w, cfg, weights(model, precision))
     plan.pcpp_set_cond(_data.cond(model))
     lat = torch.from_numpy(np.array(_data.latent(H, H))).cuda()
@@ -157,3 +157,24 @@ def test_forced_gemm_configs(cuda_ok, force, tmp_path):
     ref = oracle_run("sdxl", 32, 1, 0.0, 0, 50, "bf16", "pcpp", 2)
     for k in range(2):
         assert rel_l2(xs[k], ref[k]) <= TOL["bf16"], (force, k)
+
+
+DPM_CASES = [("tiny", 32, 2, 0.25, 1, 4, "fp32", "pcpp", 4), ("tiny", 32, 2, 0.25, 1, 4, "bf16", "pcpp", 4),
+             ("sdxl", 32, 2, 0.3, 1, 50, "bf16", "pcpp", 3)]
+
+
+@pytest.mark.parametrize("case", DPM_CASES, ids=lambda c: "-".join(map(str, c)))
+def test_dpmpp2m_path_matches_oracle(cuda_ok, case):
+    """The DPM-Solver++(2M) scheduler (north star "DDIM/DPM-solver", reading D23), fused with CFG in
+    one elementwise kernel with its x0 history per patch, follows the oracle step by step (k = 0 is
+    first order, later steps use the history)."""
+    xs, _ = lib_run(*case, scheduler="dpmpp2m")
+    ref = oracle_run(*case, scheduler="dpmpp2m")
+    tol = TOL[case[6]]
+    for k, (a, b) in enumerate(zip(xs, ref)):
+        assert rel_l2(a, b) <= tol, (k, rel_l2(a, b))
+    # and it is a different sampler: from step 1 on the DDIM trajectory is far further from the
+    # result than the GPU's own error
+    ddim = oracle_run(*case)
+    k = len(xs) - 1
+    assert rel_l2(ref[k], ddim[k]) > 3 * rel_l2(xs[k], ref[k])

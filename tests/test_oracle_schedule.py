@@ -87,3 +87,63 @@ def test_band_rows_rule():
             prev = r
     with pytest.raises(ValueError):
         S.band_rows(1.5, 8)                       # p > 1 undefined
+
+
+# ---- DPM-Solver++(2M) (north star "DDIM/DPM-solver"; reading D23) --------------------------------
+from oracle import schedule as SCH  # noqa: E402  (S is used for step counts below)
+
+def test_dpmpp_first_order_equals_ddim():
+    """The first-order DPM-Solver++ update is algebraically the DDIM (eta = 0) update."""
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((8, 8, 4))
+    e = rng.standard_normal((8, 8, 4))
+    for S, k in [(50, 0), (4, 0), (4, 3), (10, 9)]:
+        ref = SCH.ddim_step(x, e, S, k)
+        got, _ = SCH.dpmpp_2m_step(x, e, S, k, x0_prev=np.full_like(x, 1e9))   # history must be ignored
+        assert np.max(np.abs(got - ref)) <= 1e-12 * (1 + np.max(np.abs(ref)))
+
+
+def test_dpmpp_exact_on_exact_trajectory():
+    """If the model returns the true eps of x_tau = alpha x0 + sigma eps, every 2M step lands on
+    alpha' x0 + sigma' eps (x0 predictions agree, so the second-order correction vanishes)."""
+    rng = np.random.default_rng(8)
+    x0 = rng.standard_normal((4, 4, 4))
+    eps = rng.standard_normal((4, 4, 4))
+    S = 20
+    ab = SCH.alpha_bars()
+    taus = SCH.ddim_timesteps(S)
+    x = math.sqrt(ab[taus[0]]) * x0 + math.sqrt(1 - ab[taus[0]]) * eps
+    hist = None
+    for k in range(S):
+        x, hist = SCH.dpmpp_2m_step(x, eps, S, k, hist)
+        prev = taus[k] - 1000 // S
+        a = ab[prev] if prev >= 0 else ab[0]
+        assert np.max(np.abs(x - (math.sqrt(a) * x0 + math.sqrt(1 - a) * eps))) <= 1e-10
+
+
+def _one_step_errors(a, b, S):
+    """Local error of one step from tau_k (k = S/2: the same point of the ladder for every S) for
+    the "model" x0(lambda) = a + b lambda, against the closed-form solution of the data-prediction
+    ODE x'/sigma' = x/sigma + F(lambda') - F(lambda), F(lam) = e^lam (a + b (lam - 1)); the 2M
+    history is the exact x0 at the previous ladder point."""
+    ab = SCH.alpha_bars()
+    taus = SCH.ddim_timesteps(S)
+    k = S // 2
+    at, ap, aq = ab[taus[k]], ab[taus[k] - 1000 // S], ab[taus[k - 1]]
+    lt, lp, lq = SCH._lam(at), SCH._lam(ap), SCH._lam(aq)
+    F = lambda lam: math.exp(lam) * (a + b * (lam - 1.0))
+    x = np.array([0.8])
+    exact = math.sqrt(1 - ap) * (x[0] / math.sqrt(1 - at) + F(lp) - F(lt))
+    eps = (x - math.sqrt(at) * (a + b * lt)) / math.sqrt(1 - at)
+    x2, _ = SCH.dpmpp_2m_step(x, eps, S, k, np.array([a + b * lq]))
+    x1 = SCH.ddim_step(x, eps, S, k)
+    return abs(float(x2[0]) - exact), abs(float(x1[0]) - exact)
+
+
+def test_dpmpp_2m_local_order():
+    """One 2M step has local error O(h^3) (falls ~8x per halving of the step), the first-order
+    (DDIM) step O(h^2) (~4x): a dropped, mis-signed or mis-weighted history term breaks the order."""
+    e2, e1 = zip(*[_one_step_errors(0.3, -0.7, S) for S in (20, 40, 100)])
+    assert 6.0 < e2[0] / e2[1] < 10.0, e2
+    assert 3.0 < e1[0] / e1[1] < 5.0, e1
+    assert e2[2] < e1[2] / 20, (e1, e2)
