@@ -74,11 +74,16 @@ typedef struct {
   int use_graphs;             /* 1: replay per-step CUDA graphs ("CUDA Graph"); 0: eager */
   int scheduler;              /* PCPP_SCHED_DDIM (0, default) | PCPP_SCHED_DPMPP2M (1): DPM-Solver++(2M)
                                  on the same timestep ladder (north star "DDIM/DPM-solver"; DESIGN.md
-                                 reading D23).  Elementwise and patch-local: no exchange. */
+                                 reading D23) | PCPP_SCHED_ANCESTRAL (2): the DDPM ancestral sampler of
+                                 Eq. 3-4 on the same ladder (eta = 1, reading D24).
+                                 Elementwise and patch-local: no exchange. */
+  unsigned long long noise_seed; /* ANCESTRAL: key of the counter-based noise z (Philox4x64-10 on
+                                 (global latent token, step); independent of n and of the rank) */
 } pcpp_config;
 
 #define PCPP_SCHED_DDIM 0
 #define PCPP_SCHED_DPMPP2M 1
+#define PCPP_SCHED_ANCESTRAL 2
 
 #define PCPP_MAX_LAYERS 128
 

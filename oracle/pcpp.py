@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import model as M
-from .schedule import cfg_combine, ddim_step, ddim_timesteps, dpmpp_2m_step
+from .schedule import ancestral_step, cfg_combine, ddim_step, ddim_timesteps, dpmpp_2m_step, noise_patch
 
 
 @dataclass
@@ -35,7 +35,8 @@ class Config:
     steps: int = 4
     guidance: float = 5.0
     scheme: str = "pcpp"          # 'pcpp' | 'fullmap' | 'sync'
-    scheduler: str = "ddim"       # 'ddim' | 'dpmpp2m' (north star "DPM-solver", reading D23)
+    scheduler: str = "ddim"       # 'ddim' | 'dpmpp2m' (north star "DPM-solver", D23) | 'ancestral' (Eq. 3-4, D24)
+    noise_seed: int = 0           # key of the counter-based noise of the ancestral sampler (D24)
     extras: dict = field(default_factory=dict)
 
 
@@ -76,6 +77,10 @@ def sample(cfg: Config, blob: np.ndarray, x_T: np.ndarray, cond: np.ndarray,
             res = [dpmpp_2m_step(x, e, cfg.steps, k, x0p) for x, e, x0p in zip(patches, eps_hat, x0_hist)]
             patches = [r[0] for r in res]
             x0_hist = [r[1] for r in res]
+        elif cfg.scheduler == "ancestral":
+            h = patches[0].shape[0]
+            patches = [ancestral_step(x, e, cfg.steps, k, noise_patch(cfg.noise_seed, k, i * h, h, cfg.W))
+                       for i, (x, e) in enumerate(zip(patches, eps_hat))]
         else:
             patches = [ddim_step(x, e, cfg.steps, k) for x, e in zip(patches, eps_hat)]
         prev = ctx.nxt

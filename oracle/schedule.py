@@ -136,6 +136,69 @@ def dpmpp_2m_step(x: np.ndarray, eps_hat: np.ndarray, num_steps: int, k: int, x0
     return (sigma_p / sigma_t) * x - alpha_p * math.expm1(-h) * D, x0
 
 
+# ---- ancestral (DDPM, Eq. 3-4) sampling on the ladder; reading D24 ------------------------------
+PHILOX_M = (0xD2E7470EE14C6C93, 0xCA5A826395121157)
+PHILOX_W = (0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B)
+_M64 = (1 << 64) - 1
+
+
+def philox4x64_10(ctr, key):
+    """Philox4x64-10 (Salmon et al., SC'11) on a 4 x 64-bit counter and 2 x 64-bit key, in Python
+    integers.  Pinned against numpy.random.Philox (tests/test_oracle_schedule.py)."""
+    c = [int(v) & _M64 for v in ctr]
+    k0, k1 = int(key[0]) & _M64, int(key[1]) & _M64
+    for _ in range(10):
+        p0 = PHILOX_M[0] * c[0]
+        p1 = PHILOX_M[1] * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k0, p1 & _M64, (p0 >> 64) ^ c[3] ^ k1, p0 & _M64]
+        k0 = (k0 + PHILOX_W[0]) & _M64
+        k1 = (k1 + PHILOX_W[1]) & _M64
+    return c
+
+
+def noise_token(seed: int, k: int, g: int) -> np.ndarray:
+    """The 4 standard normals of latent token g (= global row * W + column) at step k (reading D24):
+    words = Philox4x64-10(counter = (g, k, 0, 0), key = (seed, 0)); Box-Muller on the word pairs
+    (w0, w1) and (w2, w3) with u = (w >> 11) * 2^-53 (u1 shifted by half an ulp so log(u1) is finite)."""
+    w = philox4x64_10((g, k, 0, 0), (seed, 0))
+    out = np.empty(4)
+    for j in range(2):
+        u1 = ((w[2 * j] >> 11) + 0.5) * 2.0 ** -53
+        u2 = (w[2 * j + 1] >> 11) * 2.0 ** -53
+        rad = math.sqrt(-2.0 * math.log(u1))
+        out[2 * j] = rad * math.cos(2.0 * math.pi * u2)
+        out[2 * j + 1] = rad * math.sin(2.0 * math.pi * u2)
+    return out
+
+
+def noise_patch(seed: int, k: int, row0: int, h: int, W: int) -> np.ndarray:
+    """z for rows [row0, row0 + h) of the [H][W][4] latent at step k (pure-Python loop: small cases)."""
+    z = np.empty((h, W, 4))
+    for r in range(h):
+        for w in range(W):
+            z[r, w] = noise_token(seed, k, (row0 + r) * W + w)
+    return z
+
+
+def ancestral_coeffs(num_steps: int, k: int):
+    """Reading D24: DDIM with eta = 1 on the D2 ladder (Song et al.: eta = 1 is the DDPM ancestral
+    sampler) -- sigma^2 = (1 - ab')/(1 - ab) (1 - ab/ab'); returns (sqrt(ab), sqrt(1-ab), sqrt(ab'),
+    sqrt(1 - ab' - sigma^2), sigma)."""
+    sa, s1a, sp, s1p = ddim_coeffs(num_steps, k)
+    a, ap = sa * sa, sp * sp
+    var = (1.0 - ap) / (1.0 - a) * (1.0 - a / ap)
+    return sa, s1a, sp, math.sqrt(max(1.0 - ap - var, 0.0)), math.sqrt(var)
+
+
+def ancestral_step(x: np.ndarray, eps_hat: np.ndarray, num_steps: int, k: int, z: np.ndarray) -> np.ndarray:
+    """x' = sqrt(ab') x0 + sqrt(1 - ab' - sigma^2) eps + sigma z,  x0 = (x - sqrt(1-ab) eps)/sqrt(ab).
+    On the full 1000-step ladder the mean is Eq. 3 and sigma^2 the posterior variance, so this
+    is Eq. 4 x_{t-1} = mu + sigma_t z."""
+    sa, s1a, sp, ce, sig = ancestral_coeffs(num_steps, k)
+    x0 = (x - s1a * eps_hat) / sa
+    return sp * x0 + ce * eps_hat + sig * z
+
+
 def ddpm_mean(x: np.ndarray, eps_hat: np.ndarray, t: int) -> np.ndarray:
     """Eq. 3 (P:67): mu = (x_t - beta_t / sqrt(1 - ab_t) eps_hat) / sqrt(alpha_t)."""
     b = betas()[t]

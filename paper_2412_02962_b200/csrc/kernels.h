@@ -97,6 +97,11 @@ void launch_cfg_ddim(const float* eps, float* latent, int h, int W, float s_cfg,
 // x0_hist <- x0.  coef[k*6 + {1/alpha, sigma, A, Bc, w0, w1}]
 void launch_cfg_dpmpp(const float* eps, float* latent, float* x0_hist, int h, int W, float s_cfg,
                       const double* coef, const int* k_dev, cudaStream_t s);
+// Eq. 2 + the ancestral sampler (Eq. 3-4 as eta = 1 on the ladder, reading D24): x <- sqrt(ab') x0 +
+// c_eps eps + sigma z, z = Box-Muller(Philox4x64-10((row0 + r) * W + w, k, 0, 0; key (seed, 0))).
+// coef[k*5 + {sqrt(ab), sqrt(1-ab), sqrt(ab'), c_eps, sigma}]; row0 = global row of the patch.
+void launch_cfg_ancestral(const float* eps, float* latent, int h, int W, int row0, float s_cfg, const double* coef,
+                          unsigned long long seed, const int* k_dev, cudaStream_t s);
 void launch_step_end(int* k_dev, cudaStream_t s);
 
 // timestep embedding: emb[b][T] for tau = taus[*k_dev]; then tproj[b][j] for all ResBlocks

@@ -120,6 +120,64 @@ void launch_cfg_dpmpp(const float* eps, float* latent, float* x0_hist, int h, in
              reinterpret_cast<float4*>(latent), reinterpret_cast<float4*>(x0_hist), h, W, s_cfg, coef, k_dev);
 }
 
+// Philox4x64-10 (Salmon et al. SC'11): counter (c0, c1, c2, c3), key (k0, k1) -> 4 x 64-bit words
+__device__ __forceinline__ void philox4x64_10(unsigned long long c[4], unsigned long long k0, unsigned long long k1) {
+  const unsigned long long M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+  const unsigned long long W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
+    const unsigned long long hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
+    const unsigned long long n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += W0; k1 += W1;
+  }
+}
+
+__global__ void cfg_ancestral_kernel(const float4* __restrict__ eps, float4* __restrict__ lat, int h, int W, int row0,
+                                     float s_cfg, const double* __restrict__ coef, unsigned long long seed,
+                                     const int* __restrict__ k_dev) {
+  pdl_trigger();
+  pdl_wait();
+  const int k = *k_dev;
+  const float sa = (float)coef[5 * k + 0], s1a = (float)coef[5 * k + 1], sp = (float)coef[5 * k + 2];
+  const float ce = (float)coef[5 * k + 3], sig = (float)coef[5 * k + 4];
+  const float inv_sa = 1.f / sa;
+  const long long n = (long long)h * W;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / W, w = i % W;
+    unsigned long long c[4] = {(unsigned long long)((row0 + r) * W + w), (unsigned long long)k, 0ull, 0ull};
+    philox4x64_10(c, seed, 0ull);
+    double z[4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {                    // Box-Muller in fp64 (reading D24)
+      const double u1 = ((double)(c[2 * j] >> 11) + 0.5) * 0x1.0p-53, u2 = (double)(c[2 * j + 1] >> 11) * 0x1.0p-53;
+      const double rad = sqrt(-2.0 * log(u1));
+      double sn, cs;
+      sincospi(2.0 * u2, &sn, &cs);
+      z[2 * j] = rad * cs; z[2 * j + 1] = rad * sn;
+    }
+    const float4 eu = eps[(r * 2 + 0) * W + w], ec = eps[(r * 2 + 1) * W + w];
+    float4 x = lat[i];
+    const float e[4] = {eu.x + s_cfg * (ec.x - eu.x), eu.y + s_cfg * (ec.y - eu.y),
+                        eu.z + s_cfg * (ec.z - eu.z), eu.w + s_cfg * (ec.w - eu.w)};
+    float* xv = &x.x;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const float x0 = (xv[cc] - s1a * e[cc]) * inv_sa;
+      xv[cc] = sp * x0 + ce * e[cc] + sig * (float)z[cc];
+    }
+    lat[i] = x;
+  }
+}
+void launch_cfg_ancestral(const float* eps, float* latent, int h, int W, int row0, float s_cfg, const double* coef,
+                          unsigned long long seed, const int* k_dev, cudaStream_t s) {
+  const long long n = (long long)h * W;
+  int blocks = (int)((n + 255) / 256); if (blocks > 1184) blocks = 1184;
+  launch_pdl(cfg_ancestral_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const float4*>(eps),
+             reinterpret_cast<float4*>(latent), h, W, row0, s_cfg, coef, seed, k_dev);
+}
+
 __global__ void step_end_kernel(int* k_dev) {
   pdl_trigger();
   pdl_wait(); *k_dev += 1; }

@@ -40,8 +40,8 @@ pcpp_status validate(int H, int W, int C, int n, double p, int w, const pcpp_con
   if (n > 1 && w < 1) { set_error("warmup_steps must be >= 1 when n > 1 (reading D20)"); return PCPP_ERR_INVALID; }
   if (w < 0 || w > cfg->num_steps) { set_error("warmup_steps must be in [0, num_steps]"); return PCPP_ERR_INVALID; }
   if (cfg->guidance_scale < 1.0f) { set_error("guidance_scale must be >= 1 (Eq. 2, P:39)"); return PCPP_ERR_INVALID; }
-  if (cfg->scheduler != PCPP_SCHED_DDIM && cfg->scheduler != PCPP_SCHED_DPMPP2M) {
-    set_error("scheduler must be PCPP_SCHED_DDIM or PCPP_SCHED_DPMPP2M"); return PCPP_ERR_INVALID;
+  if (cfg->scheduler != PCPP_SCHED_DDIM && cfg->scheduler != PCPP_SCHED_DPMPP2M && cfg->scheduler != PCPP_SCHED_ANCESTRAL) {
+    set_error("scheduler must be PCPP_SCHED_DDIM, PCPP_SCHED_DPMPP2M or PCPP_SCHED_ANCESTRAL"); return PCPP_ERR_INVALID;
   }
   if (cfg->precision != PCPP_FP32 && cfg->precision != PCPP_BF16) { set_error("bad precision"); return PCPP_ERR_INVALID; }
   if (cfg->scheme < 0 || cfg->scheme > 2) { set_error("bad scheme"); return PCPP_ERR_INVALID; }

@@ -121,6 +121,7 @@ pcpp_status plan_allocate(Plan& P) {
   P.tproj = (float*)galloc((size_t)2 * P.J * 4); P.cond = (float*)galloc(P.T * 4);
   P.taus = (int*)galloc(P.S * 4); P.coef = (double*)galloc(P.S * 4 * 8); P.k_dev = (int*)galloc(16);
   P.coef_dpm = (double*)galloc(P.S * 6 * 8);
+  P.coef_anc = (double*)galloc(P.S * 5 * 8);
   if (P.cfg.scheduler == PCPP_SCHED_DPMPP2M) P.x0_hist = (float*)galloc((size_t)P.nr * (P.H / P.n) * P.W * 4 * 4);
   if (P.dtype == DT_BF16) {       // split-K workspace: up to 8 fp32 partial copies of the largest GEMM output
     size_t mx = 0;
@@ -176,6 +177,15 @@ pcpp_status plan_allocate(Plan& P) {
     cd[6 * k + 4] = w0; cd[6 * k + 5] = w1;
   }
   CK(cudaMemcpy(P.coef_dpm, cd.data(), P.S * 6 * 8, cudaMemcpyHostToDevice));
+  // ancestral sampler (reading D24): eta = 1, sigma^2 = (1 - ab')/(1 - ab) (1 - ab/ab')
+  std::vector<double> ca(5 * P.S);
+  for (int k = 0; k < P.S; ++k) {
+    const double at = coef[4 * k + 0] * coef[4 * k + 0], ap = coef[4 * k + 2] * coef[4 * k + 2];
+    const double var = (1.0 - ap) / (1.0 - at) * (1.0 - at / ap);
+    ca[5 * k + 0] = coef[4 * k + 0]; ca[5 * k + 1] = coef[4 * k + 1]; ca[5 * k + 2] = coef[4 * k + 2];
+    ca[5 * k + 3] = std::sqrt(std::max(1.0 - ap - var, 0.0)); ca[5 * k + 4] = std::sqrt(var);
+  }
+  CK(cudaMemcpy(P.coef_anc, ca.data(), P.S * 5 * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(P.taus, taus.data(), P.S * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(P.coef, coef.data(), P.S * 4 * 8, cudaMemcpyHostToDevice));
   return PCPP_OK;
@@ -644,7 +654,10 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
         const int h = P.H / n;
         for (int vr = 0; vr < nr; ++vr) {
           float* lat = latent + (P.loopback ? (size_t)vr * h * P.W * 4 : 0);
-          if (P.cfg.scheduler == PCPP_SCHED_DPMPP2M)
+          if (P.cfg.scheduler == PCPP_SCHED_ANCESTRAL)
+            launch_cfg_ancestral(reinterpret_cast<const float*>(view(P, vr, op.in0, par).base), lat, h, P.W,
+                                 (P.rank0 + vr) * h, P.cfg.guidance_scale, P.coef_anc, P.cfg.noise_seed, P.k_dev, s);
+          else if (P.cfg.scheduler == PCPP_SCHED_DPMPP2M)
             launch_cfg_dpmpp(reinterpret_cast<const float*>(view(P, vr, op.in0, par).base), lat,
                              P.x0_hist + (size_t)vr * h * P.W * 4, h, P.W, P.cfg.guidance_scale, P.coef_dpm, P.k_dev, s);
           else

@@ -109,6 +109,7 @@ struct Plan {
   int* taus = nullptr; double* coef = nullptr; int* k_dev = nullptr;
   double* coef_dpm = nullptr;   // DPM-Solver++(2M): [S][6] {1/alpha, sigma, sigma'/sigma, -alpha'(e^-h - 1), w0, w1}
   float* x0_hist = nullptr;     // DPM-Solver++(2M) data-prediction history, [nr][h][W][4] fp32
+  double* coef_anc = nullptr;   // ancestral (eta = 1): [S][5] {sqrt(ab), sqrt(1-ab), sqrt(ab'), c_eps, sigma}
   float* ws = nullptr; size_t ws_elems = 0;   // split-K workspace
   std::vector<cudaEvent_t> op_ev; bool op_ev_on = false;   // per-op timing (PCPP_OP_TIMING, pcpp_profile)
   std::vector<void*> gallocs;

@@ -22,7 +22,7 @@ MODELS = {"tiny": MODEL_TINY, "sdxl": MODEL_SDXL}
 SCHEMES = {"pcpp": SCHEME_PCPP, "fullmap": SCHEME_FULLMAP, "sync": SCHEME_SYNC}
 
 
-SCHEDULERS = {"ddim": 0, "dpmpp2m": 1}   # PCPP_SCHED_* (include/pcpp.h)
+SCHEDULERS = {"ddim": 0, "dpmpp2m": 1, "ancestral": 2}   # PCPP_SCHED_* (include/pcpp.h)
 
 
 class pcpp_config(C.Structure):
@@ -30,7 +30,8 @@ class pcpp_config(C.Structure):
                 ("guidance_scale", C.c_float), ("precision", C.c_int), ("scheme", C.c_int),
                 ("model", C.c_int), ("weights", C.POINTER(C.c_float)), ("weights_len", C.c_size_t),
                 ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("comm_backend", C.c_int),
-                ("kernels", C.c_int), ("use_graphs", C.c_int), ("scheduler", C.c_int)]
+                ("kernels", C.c_int), ("use_graphs", C.c_int), ("scheduler", C.c_int),
+                ("noise_seed", C.c_ulonglong)]
 
 
 class pcpp_info(C.Structure):
@@ -152,7 +153,7 @@ def pcpp_get_unique_id() -> bytes:
 
 def make_config(model="sdxl", num_steps=50, guidance=5.0, precision="bf16", scheme="pcpp",
                 backend="loopback", rank=0, world=1, weights=None, nccl_id=None, stream=None,
-                kernels="auto", graphs=True, scheduler="ddim"):
+                kernels="auto", graphs=True, scheduler="ddim", noise_seed=0):
     cfg = pcpp_config()
     lib().pcpp_config_default(C.byref(cfg))
     cfg.model = MODELS[model]
@@ -165,6 +166,7 @@ def make_config(model="sdxl", num_steps=50, guidance=5.0, precision="bf16", sche
     cfg.kernels = KERNELS_AUTO if kernels == "auto" else KERNELS_SIMT
     cfg.use_graphs = 1 if graphs else 0
     cfg.scheduler = SCHEDULERS[scheduler]
+    cfg.noise_seed = noise_seed
     if weights is not None:
         cfg.weights = weights.ctypes.data_as(C.POINTER(C.c_float))
         cfg.weights_len = weights.size

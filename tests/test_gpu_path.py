@@ -27,16 +27,18 @@ def weights(model, precision):
 
 
 @functools.lru_cache(maxsize=None)
-def oracle_run(model, H, n, p, w, S, precision, scheme, max_steps, scheduler="ddim"):
-    cfg = OP.Config(model=model, H=H, W=H, n=n, p=p, warmup=w, steps=S, scheme=scheme, scheduler=scheduler)
+def oracle_run(model, H, n, p, w, S, precision, scheme, max_steps, scheduler="ddim", noise_seed=0):
+    cfg = OP.Config(model=model, H=H, W=H, n=n, p=p, warmup=w, steps=S, scheme=scheme, scheduler=scheduler,
+                    noise_seed=noise_seed)
     out = OP.sample(cfg, weights(model, precision), _data.latent(H, H), _data.cond(model), max_steps=max_steps)
     return out["xs"]
 
 
-def lib_run(model, H, n, p, w, S, precision, scheme, max_steps, kernels="auto", graphs=True, scheduler="ddim"):
+def lib_run(model, H, n, p, w, S, precision, scheme, max_steps, kernels="auto", graphs=True, scheduler="ddim",
+            noise_seed=0):
     import torch
     cfg = pcpp.make_config(model=model, num_steps=S, precision=precision, scheme=scheme, kernels=kernels,
-                           graphs=graphs, scheduler=scheduler)
+                           graphs=graphs, scheduler=scheduler, noise_seed=noise_seed)
     plan = pcpp.Plan(H, H, 4, n, p, w, cfg, weights(model, precision))
     plan.pcpp_set_cond(_data.cond(model))
     lat = torch.from_numpy(np.array(_data.latent(H, H))).cuda()
@@ -178,3 +180,17 @@ def test_dpmpp2m_path_matches_oracle(cuda_ok, case):
     ddim = oracle_run(*case)
     k = len(xs) - 1
     assert rel_l2(ref[k], ddim[k]) > 3 * rel_l2(xs[k], ref[k])
+
+
+@pytest.mark.parametrize("case", DPM_CASES, ids=lambda c: "-".join(map(str, c)))
+def test_ancestral_path_matches_oracle(cuda_ok, case):
+    """The ancestral sampler (Eq. 3-4 on the ladder, reading D24): the kernel's Philox4x64-10 +
+    Box-Muller noise for each global latent token and step equals the oracle's, so the stochastic
+    trajectories agree step by step; another seed gives another trajectory."""
+    xs, _ = lib_run(*case, scheduler="ancestral", noise_seed=11)
+    ref = oracle_run(*case, scheduler="ancestral", noise_seed=11)
+    tol = TOL[case[6]]
+    for k, (a, b) in enumerate(zip(xs, ref)):
+        assert rel_l2(a, b) <= tol, (k, rel_l2(a, b))
+    other = oracle_run(*case, scheduler="ancestral", noise_seed=12)
+    assert rel_l2(ref[0], other[0]) > 3 * rel_l2(xs[0], ref[0])

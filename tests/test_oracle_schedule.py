@@ -147,3 +147,41 @@ def test_dpmpp_2m_local_order():
     assert 6.0 < e2[0] / e2[1] < 10.0, e2
     assert 3.0 < e1[0] / e1[1] < 5.0, e1
     assert e2[2] < e1[2] / 20, (e1, e2)
+
+
+# ---- ancestral sampler (Eq. 3-4; reading D24) ------------------------------------------------------
+
+def test_philox_matches_numpy():
+    """The oracle's Philox4x64-10 equals numpy's Philox bit generator (which advances its counter
+    before each block: Philox(counter=c) produces philox(c + 1))."""
+    for key, ctr in [((5, 0), (0, 0, 0, 0)), ((2**63 + 12345, 77), (41, 3, 0, 0)), ((0, 0), (2**64 - 2, 9, 1, 0))]:
+        bg = np.random.Philox(key=np.array(key, dtype=np.uint64), counter=np.array(ctr, dtype=np.uint64))
+        want = [int(v) for v in bg.random_raw(4)]
+        c1 = list(ctr)
+        c1[0] = (c1[0] + 1) % 2**64
+        if c1[0] == 0:
+            c1[1] += 1
+        assert SCH.philox4x64_10(c1, key) == want
+
+
+def test_noise_is_standard_normal():
+    z = np.concatenate([SCH.noise_token(3, k, g) for k in range(4) for g in range(2500)])
+    assert abs(z.mean()) < 0.03 and abs(z.std() - 1.0) < 0.03
+    assert abs(np.mean(z ** 4) - 3.0) < 0.2                    # Gaussian kurtosis
+    assert SCH.noise_token(3, 1, 7).tolist() != SCH.noise_token(3, 2, 7).tolist()
+
+
+def test_ancestral_reduces_to_eq3_eq4_on_full_ladder():
+    """With S = 1000 (adjacent timesteps) the eta = 1 update's mean is Eq. 3's mu and its variance
+    the DDPM posterior variance (1 - ab_{t-1})/(1 - ab_t) beta_t: the sampler is Eq. 4."""
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((4, 4, 4))
+    e = rng.standard_normal((4, 4, 4))
+    ab = SCH.alpha_bars()
+    be = SCH.betas()
+    for k in (1, 500, 998):                     # tau_0 = 1000 lies past the 1000-entry table
+        t = SCH.ddim_timesteps(1000)[k]
+        mean = SCH.ancestral_step(x, e, 1000, k, np.zeros_like(x))
+        np.testing.assert_allclose(mean, SCH.ddpm_mean(x, e, t), rtol=1e-9, atol=1e-9)
+        sig = SCH.ancestral_coeffs(1000, k)[4]
+        assert abs(sig ** 2 - (1 - ab[t - 1]) / (1 - ab[t]) * be[t]) <= 1e-12
