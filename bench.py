@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-loopback", action="store_true", help="skip the n = 2/4/8 loopback projection (N = 1)")
     ap.add_argument("--kernels", default="auto", choices=["auto", "simt"])
     return ap.parse_args()
 
@@ -314,6 +315,43 @@ def main():
                          f"({times[0]:.1f} s), extrapolated x{scale:.1f} by the algorithmic-flop ratio"}
 
     plan.close()
+
+    # Single-GPU view of the partially conditioned path at the bench scale: all n virtual ranks of an
+    # n-patch plan run back to back on this GPU (loopback backend: exchanges are device copies of
+    # exactly the bytes NCCL would move).  ms/step of all ranks / n = the mean per-rank step (an
+    # upper bound on a rank's compute on its own GPU); a projection, not a multi-GPU measurement.
+    loop = None
+    if rank == 0 and world == 1 and not args.no_loopback and args.scheme == "pcpp" and args.res == 128:
+        loop = {}
+        blob2 = inputs.make_weight_blob(inputs.init_specs(pcpp.manifest("sdxl")))
+        for nv in (2, 4, 8):
+            pv, wv = P_BY_N[nv], 4                 # the paper's 4 synchronous warm-up steps
+            cfg2 = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme="pcpp", backend="loopback",
+                                    kernels=args.kernels)
+            pl = pcpp.Plan(H, W, 4, nv, pv, wv, cfg2, blob2)
+            pl.pcpp_set_cond(cond)
+            lat2 = torch.from_numpy(np.ascontiguousarray(xT)).cuda()
+            pl.pcpp_reset()
+            for k in range(wv + 2):
+                pl.pcpp_step(lat2, k)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for k in range(wv + 2, wv + 7):
+                pl.pcpp_step(lat2, k)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 5
+            inf2 = pl.pcpp_query()
+            pl.close()
+            loop[f"n{nv}"] = {"p": pv, "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / nv, 4),
+                              "projected_speedup_vs_n1": round(ms / (t / nv), 2),
+                              "step_flops_rank_max": inf2["step_flops_rank_max"],
+                              "bytes_exchanged_per_step": sum(inf2["bytes_counted_async"])}
+        loop["note"] = ("loopback: the n virtual ranks run sequentially on one GPU, exchanges are device copies; "
+                        "ms_per_rank = all-rank time / n (a projection of one rank on its own GPU, not measured)")
+        del blob2
+
     if rank == 0:
         cls = ("attn", "conv", "gn")
         out = {
@@ -335,6 +373,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e, "roofline": roof, "roofline_attention": roof_attn, "cpu_baseline": cpu,
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in prof.items()},
+            "pcpp_loopback_1gpu": loop,
             "context": "paper: 2.36-8.02x speed-up on 4-8 A100-40GB, SDXL fp16 (P:5); not comparable hardware",
         }
         print(json.dumps(out), flush=True)
