@@ -194,3 +194,26 @@ def test_ancestral_path_matches_oracle(cuda_ok, case):
         assert rel_l2(a, b) <= tol, (k, rel_l2(a, b))
     other = oracle_run(*case, scheduler="ancestral", noise_seed=12)
     assert rel_l2(ref[0], other[0]) > 3 * rel_l2(xs[0], ref[0])
+
+
+def test_nccl_backend_single_rank_matches_loopback(cuda_ok):
+    """The NCCL backend (communicator init, graph capture with the comm stream, the final x_0
+    all-gather of pcpp_sample) at world = 1 reproduces the loopback backend bitwise."""
+    import torch
+    blob = weights("tiny", "bf16")
+    cond = _data.cond("tiny")
+    xT = np.array(_data.latent(32, 32), dtype=np.float32)          # writable copy
+    outs = []
+    for backend in ("loopback", "nccl"):
+        kw = {}
+        if backend == "nccl":
+            kw = dict(rank=0, world=1, nccl_id=pcpp.pcpp_get_unique_id())
+        cfg = pcpp.make_config(model="tiny", num_steps=4, precision="bf16", backend=backend, **kw)
+        plan = pcpp.Plan(32, 32, 4, 1, 0.0, 0, cfg, blob)
+        x0 = torch.empty((32, 32, 4), dtype=torch.float32).pin_memory()
+        xt = torch.from_numpy(xT).pin_memory()
+        ch = torch.from_numpy(np.ascontiguousarray(cond, dtype=np.float32)).pin_memory()
+        plan.pcpp_sample_into(xt.data_ptr(), ch.data_ptr(), x0.data_ptr())
+        outs.append(x0.numpy().copy())
+        plan.close()
+    assert np.array_equal(outs[0], outs[1])
