@@ -1,7 +1,9 @@
 // tcgen05 flash attention for partially conditioned attention (§3.3; Fig. 3), sm_100a.
 //
 // One CTA = NWG x 128 query tokens of one (batch b, head): NWG = 1 (default, two CTAs per SM) or
-// NWG = 2 (one CTA per SM, two softmax warpgroups ping-pong on one K/V stream).  Q comes from the local fresh patch; the
+// NWG = 2 (one CTA per SM, two softmax warpgroups ping-pong on one K/V stream).  With NWG = 1 the
+// probabilities P go to TMEM (packed bf16, columns 192-255) and O += P V is a TS MMA (A from TMEM),
+// which frees the shared memory for a 3-stage K/V ring.  Q comes from the local fresh patch; the
 // key/value stream is the concatenation of up to three row sources [stale top band ; local fresh ;
 // stale bottom band] (Eq. 1; reading D13), each a [rows][B][W][2C] tensor read in place -- the
 // neighbour bands straight out of the receive buffers, no concat copy.
@@ -36,12 +38,13 @@ constexpr int TILE = 128 * 128;              // bytes of one 128-token x 64-dim 
 // ping-pong on one K/V stream.  NWG = 1: two CTAs per SM (TMEM 2 x 256 columns, smem 2 x 112 KB),
 // the ping-pong happens between CTAs and the grid has twice the granularity (shorter tail wave).
 template <int NWG> struct AttnCfg {
-  static constexpr int KST = NWG == 2 ? 3 : 2;                 // K/V pipeline stages
+  static constexpr bool P_TMEM = NWG == 1;                     // NWG = 1: P lives in TMEM (cols 192-255)
+  static constexpr int KST = 3;                                // K/V pipeline stages
   static constexpr int SM_Q = 0;                               // NWG query tiles
   static constexpr int SM_K = NWG * TILE;                      // KST stages
   static constexpr int SM_V = SM_K + KST * TILE;               // KST stages
-  static constexpr int SM_P = SM_V + KST * TILE;               // NWG x (2 x 16 KB atoms: keys 0-63, 64-127)
-  static constexpr int SM_BAR = SM_P + NWG * 2 * TILE;
+  static constexpr int SM_P = SM_V + KST * TILE;               // NWG x (2 x 16 KB atoms: keys 0-63, 64-127), smem P only
+  static constexpr int SM_BAR = SM_P + (P_TMEM ? 0 : NWG * 2 * TILE);
   static constexpr int ALIGN_SLACK = NWG == 2 ? 1024 : 0;       // NWG = 1: the dynamic base must be 1 KB aligned
   static constexpr int SMEM = ALIGN_SLACK + SM_BAR + 128;
   static constexpr int THREADS = 64 + 128 * NWG;               // warp 0 TMA, warp 1 MMA, NWG softmax warpgroups
@@ -169,8 +172,12 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
       auto issue_o = [&](int g, int st, bool first) {
         const uint64_t pd = p_desc + (uint64_t)((g * 2 * TILE) >> 4), vd = v_desc + (uint64_t)((st * TILE) >> 4);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          sm100::mma_bf16_ss(tmem + NWG * 128 + g * 64, pd + (k >> 2) * 1024 + (k & 3) * 2, vd + k * 128, id_o, (!first || k != 0) ? 1u : 0u);
+        for (int k = 0; k < 8; ++k) {
+          if constexpr (Cfg::P_TMEM)       // A = P from TMEM: 16 keys = 8 packed columns per MMA
+            sm100::mma_bf16_ts(tmem + NWG * 128 + g * 64, tmem + 192 + k * 8, vd + k * 128, id_o, (!first || k != 0) ? 1u : 0u);
+          else
+            sm100::mma_bf16_ss(tmem + NWG * 128 + g * 64, pd + (k >> 2) * 1024 + (k & 3) * 2, vd + k * 128, id_o, (!first || k != 0) ? 1u : 0u);
+        }
         sm100::mma_commit(&o_full[g]);
       };
       if (nt > 0) {
@@ -209,6 +216,7 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
       const float sl2 = 0.125f * 1.4426950408889634f;   // 1/sqrt(64) * log2(e)
       float m = -INFINITY, l = 0.f;
       uint8_t* P = smem + SM_P + g * 2 * TILE;
+      const uint32_t t_p = trow + 192;                 // P_TMEM: packed P columns [192, 256)
       int s, r0, w0;
       tile_coords(p, j0, s, r0, w0);            // then walked incrementally, like the producer
       for (int j = 0; j < nt; ++j) {
@@ -270,8 +278,19 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
           float pv[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) { pv[i] = fast_exp2(fmaf(sv[i], sl2, -m_new)); ls += pv[i]; }
-          const int atom = key0 >> 6, chunk = (key0 & 63) >> 3;
-          store8(reinterpret_cast<bf16*>(P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4)), pv);
+          if constexpr (Cfg::P_TMEM) {     // keys key0..key0+7 -> 4 packed bf16x2 columns of this row
+            uint32_t u[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(pv[2 * i], pv[2 * i + 1]);
+              u[i] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+                         :: "r"(t_p + (key0 >> 1)), "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]) : "memory");
+          } else {
+            const int atom = key0 >> 6, chunk = (key0 & 63) >> 3;
+            store8(reinterpret_cast<bf16*>(P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4)), pv);
+          }
         };
 #pragma unroll
         for (int u = 0; u < 4; ++u) emit8(lo + 8 * u, 32 + 8 * u);           // cols 32-63 (still in lo)
@@ -290,7 +309,8 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
         for (int u = 0; u < 8; ++u) emit8(hi + 8 * u, 64 + 8 * u);            // cols 64-127
         l = l * alpha + ls;
         m = m_new;
-        sm100::fence_proxy_async_smem();
+        if constexpr (Cfg::P_TMEM) sm100::tmem_wait_st();
+        else sm100::fence_proxy_async_smem();
         sm100::fence_before();
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&p_full[g]);     // one arrival per warp
