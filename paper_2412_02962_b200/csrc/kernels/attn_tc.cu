@@ -274,19 +274,19 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
         }
         // pass 2: p = exp2(s * scale - m) -> bf16 P (K-major SW128 smem), row sum
         float ls = 0.f;
+        uint32_t pk16[16];
         auto emit8 = [&](const float* sv, int key0) {
           float pv[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) { pv[i] = fast_exp2(fmaf(sv[i], sl2, -m_new)); ls += pv[i]; }
-          if constexpr (Cfg::P_TMEM) {     // keys key0..key0+7 -> 4 packed bf16x2 columns of this row
-            uint32_t u[4];
+          if constexpr (Cfg::P_TMEM) {     // keys key0..key0+7 -> 4 packed bf16x2 columns, stored 16 at a time
+            const int q4 = (key0 >> 3) & 3;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               __nv_bfloat162 h2 = __floats2bfloat162_rn(pv[2 * i], pv[2 * i + 1]);
-              u[i] = *reinterpret_cast<uint32_t*>(&h2);
+              pk16[q4 * 4 + i] = *reinterpret_cast<uint32_t*>(&h2);
             }
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
-                         :: "r"(t_p + (key0 >> 1)), "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]) : "memory");
+            if (q4 == 3) sm100::tmem_st16(t_p + ((key0 >> 1) & ~15), pk16);
           } else {
             const int atom = key0 >> 6, chunk = (key0 & 63) >> 3;
             store8(reinterpret_cast<bf16*>(P + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4)), pv);
