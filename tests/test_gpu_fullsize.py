@@ -100,3 +100,30 @@ def test_groupnorm_fullsize(cuda_ok, shape):
     np.testing.assert_allclose(m.cpu().numpy(), ctx.nxt[("gn0", "m")][0], rtol=1e-6, atol=1e-3)
     got = np.transpose(y.float().cpu().numpy(), (1, 0, 2, 3))
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-2
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_bench_workload_bf16_matches_fp32_path(cuda_ok, n):
+    """The bench's whole 1024^2 step, in the launch configuration bench.py times (tcgen05 kernels,
+    GEMM table profiles/gemm_tune_b200.txt, CUDA graphs), against the same plan in fp32 with the
+    SIMT kernels -- the path the oracle parity tests pin at small sizes: one DDIM step (and, for
+    n = 2, the warm-up then an async step with stale bands) agree to the bf16 tolerance."""
+    import torch
+    blob = inputs.make_weight_blob(inputs.init_specs(pcpp.manifest("sdxl")))
+    xT = np.array(inputs.make_latent(128, 128), dtype=np.float32)
+    cond = inputs.make_cond(1280)
+    p, w = (0.0, 0) if n == 1 else (0.3, 1)
+    steps = 1 if n == 1 else 2
+    outs = {}
+    for prec, kern in (("bf16", "auto"), ("fp32", "simt")):
+        cfg = pcpp.make_config(model="sdxl", num_steps=50, precision=prec, kernels=kern)
+        plan = pcpp.Plan(128, 128, 4, n, p, w, cfg, blob)
+        plan.pcpp_set_cond(cond)
+        lat = torch.from_numpy(xT.copy()).cuda()
+        for k in range(steps):
+            plan.pcpp_step(lat, k)
+        torch.cuda.synchronize()
+        outs[prec] = lat.cpu().numpy().astype(np.float64)
+        plan.close()
+    err = float(np.linalg.norm(outs["bf16"] - outs["fp32"]) / np.linalg.norm(outs["fp32"]))
+    assert err <= 2e-2, err
