@@ -116,5 +116,7 @@ struct CopySeg { const void* src; void* dst; unsigned long long bytes; };
 void launch_copy_segments(const CopySeg* segs_dev, int nseg, unsigned long long max_bytes, cudaStream_t s);
 
 void launch_memset_zero(void* p, size_t bytes, cudaStream_t s);
+// one thread spinning ~cycles clocks (delay injection on the comm stream, tests only)
+void launch_spin(long long cycles, cudaStream_t s);
 
 }  // namespace pcpp

@@ -276,4 +276,10 @@ void launch_copy_segments(const CopySeg* segs_dev, int nseg, unsigned long long 
 
 void launch_memset_zero(void* p, size_t bytes, cudaStream_t s) { cudaMemsetAsync(p, 0, bytes, s); }
 
+__global__ void spin_kernel(long long cycles) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {}
+}
+void launch_spin(long long cycles, cudaStream_t s) { spin_kernel<<<1, 1, 0, s>>>(cycles); }
+
 }  // namespace pcpp

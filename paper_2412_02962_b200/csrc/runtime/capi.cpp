@@ -1,3 +1,4 @@
+#include <cstdlib>
 // extern "C" boundary of libpcpp (include/pcpp.h).  No exception crosses it.
 #include <cmath>
 #include <cstring>
@@ -142,6 +143,8 @@ static pcpp_status setup_plan(Plan& P, int H, int W, int C, int n, double p, int
   P.cfg = *cfg; P.H = H; P.W = W; P.C = C; P.n = n; P.p = p; P.warmup = w; P.S = cfg->num_steps;
   P.dtype = cfg->precision == PCPP_FP32 ? DT_F32 : DT_BF16;
   P.loopback = cfg->comm_backend == PCPP_COMM_LOOPBACK || n == 1;
+  P.xasync = P.loopback && n > 1 && getenv("PCPP_LOOPBACK_ASYNC") && atoi(getenv("PCPP_LOOPBACK_ASYNC")) != 0;
+  P.xdelay = (P.xasync && getenv("PCPP_XCH_DELAY")) ? atoll(getenv("PCPP_XCH_DELAY")) : 0;
   P.nr = P.loopback ? n : 1;
   P.rank0 = P.loopback ? 0 : cfg->rank;
   return build_program(P, cfg->model);
@@ -229,7 +232,7 @@ static pcpp_status step_internal(pcpp_plan_s* h, float* latent, int t) {
   if (t != P.k || t >= P.S) { set_error("pcpp_step(t=%d) but the plan is at step %d of %d", t, P.k, P.S); return PCPP_ERR_STATE; }
   const int sync = (P.n > 1 && (P.cfg.scheme == PCPP_SCHEME_SYNC || t < P.warmup)) ? 1 : 0;
   const int par = t & 1;
-  const bool fork = !P.loopback && P.n > 1;
+  const bool fork = (!P.loopback || P.xasync) && P.n > 1;
   pcpp_status st = PCPP_OK;
   cudaError_t e;
   if (P.cfg.use_graphs) {
@@ -346,7 +349,7 @@ pcpp_status pcpp_profile(pcpp_plan_t h, float* latent, int kind, int sync, int i
   Plan& P = *h->P;
   if (P.poisoned) { set_error("plan is poisoned"); return PCPP_ERR_STATE; }
   sync = (P.n > 1 && sync) ? 1 : 0;
-  const bool fork = !P.loopback && P.n > 1;
+  const bool fork = (!P.loopback || P.xasync) && P.n > 1;
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge = nullptr;
   CKS(cudaStreamSynchronize(P.s0));

@@ -408,6 +408,18 @@ pcpp_status plan_init_comm(Plan& P) {
 
 static pcpp_status exchange(Plan& P, int xo, int sync, int par) {
   const XGroup& G = P.xg[sync][par][xo];
+  if (P.loopback && P.xasync) {      // the NCCL protocol with device copies (test mode)
+    const auto& sr = P.seg_remote[sync][par][xo];
+    CK(cudaEventRecord(P.ev_x, P.s0));
+    CK(cudaStreamWaitEvent(P.s1, P.ev_x, 0));
+    if (P.xdelay) launch_spin(P.xdelay * 1000 * (1 + (xo * 7919 + par * 31 + sync) % 5), P.s1);
+    launch_copy_segments(P.segs_dev + sr.first, sr.count, sr.maxb, P.s1);
+    if (G.wait) {
+      CK(cudaEventRecord(P.ev_x, P.s1));
+      CK(cudaStreamWaitEvent(P.s0, P.ev_x, 0));
+    }
+    return PCPP_OK;
+  }
   if (P.loopback) {
     const auto& sr = P.seg_remote[sync][par][xo];
     launch_copy_segments(P.segs_dev + sr.first, sr.count, sr.maxb, P.s0);

@@ -77,6 +77,10 @@ struct Plan {
   int nr = 1;            // virtual ranks held here (n for loopback, 1 for NCCL)
   int rank0 = 0;         // global rank of virtual rank 0
   bool loopback = true;
+  // loopback test mode (PCPP_LOOPBACK_ASYNC=1): the exchange copies run on the comm stream S1 with the
+  // NCCL backend's event protocol (one step of slack), optionally behind a per-exchange spin of
+  // PCPP_XCH_DELAY x (1..5) k-cycles (delay injection: the results must not change)
+  bool xasync = false; long long xdelay = 0;
   bool use_tc = false;
 
   // program

@@ -217,3 +217,24 @@ def test_nccl_backend_single_rank_matches_loopback(cuda_ok):
         outs.append(x0.numpy().copy())
         plan.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("case", [("tiny", 32, 2, 0.25, 1, 4, "bf16", "pcpp", 4), ("tiny", 32, 4, 0.5, 1, 4, "fp32", "pcpp", 4),
+                                  ("tiny", 32, 4, 0.5, 2, 4, "bf16", "fullmap", 4)], ids=lambda c: "-".join(map(str, c)))
+@pytest.mark.parametrize("delay", ["0", "60"])
+def test_async_exchange_protocol_bitwise(cuda_ok, case, delay):
+    """SURVEY §4.6 race / ordering check on one GPU: with PCPP_LOOPBACK_ASYNC the exchanges run on the
+    comm stream with the NCCL backend's event protocol (issued behind the producer, consumed one step
+    later, parity buffers, fork / join in the captured step graph), optionally behind an injected
+    per-exchange delay of 60-300 k cycles; the trajectory is bitwise the synchronous loopback's."""
+    import os
+    ref, _ = lib_run(*case)
+    os.environ["PCPP_LOOPBACK_ASYNC"] = "1"
+    os.environ["PCPP_XCH_DELAY"] = delay
+    try:
+        got, _ = lib_run(*case)
+    finally:
+        del os.environ["PCPP_LOOPBACK_ASYNC"]
+        del os.environ["PCPP_XCH_DELAY"]
+    for k, (a, b) in enumerate(zip(got, ref)):
+        assert np.array_equal(a, b), k
