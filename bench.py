@@ -324,9 +324,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_loopback and args.scheme == "pcpp" and args.res == 128:
         loop = {}
         blob2 = inputs.make_weight_blob(inputs.init_specs(pcpp.manifest("sdxl")))
-        for nv in (2, 4, 8):
+        for nv, sch in ((2, "pcpp"), (4, "pcpp"), (8, "pcpp"), (8, "fullmap")):
             pv, wv = P_BY_N[nv], 4                 # the paper's 4 synchronous warm-up steps
-            cfg2 = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme="pcpp", backend="loopback",
+            cfg2 = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme=sch, backend="loopback",
                                     kernels=args.kernels)
             pl = pcpp.Plan(H, W, 4, nv, pv, wv, cfg2, blob2)
             pl.pcpp_set_cond(cond)
@@ -344,12 +344,14 @@ def main():
             t = e0.elapsed_time(e1) / 5
             inf2 = pl.pcpp_query()
             pl.close()
-            loop[f"n{nv}"] = {"p": pv, "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / nv, 4),
+            loop[f"n{nv}" + ("" if sch == "pcpp" else "_fullmap")] = {
+                              "scheme": sch, "p": pv, "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / nv, 4),
                               "projected_speedup_vs_n1": round(ms / (t / nv), 2),
                               "step_flops_rank_max": inf2["step_flops_rank_max"],
                               "bytes_exchanged_per_step": sum(inf2["bytes_counted_async"])}
         loop["note"] = ("loopback: the n virtual ranks run sequentially on one GPU, exchanges are device copies; "
-                        "ms_per_rank = all-rank time / n (a projection of one rank on its own GPU, not measured)")
+                        "ms_per_rank = all-rank time / n (a projection of one rank on its own GPU, not measured); "
+                        "n8_fullmap = the DistriFusion-style full-map exchange (P:86) on the same kernels")
         del blob2
 
     if rank == 0:
