@@ -41,6 +41,14 @@ template <> __device__ __forceinline__ float from_f<float>(float x) { return x; 
 template <> __device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
 
 __device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
+// SiLU with one MUFU op: x sigmoid(x) = 0.5 x (1 + tanh(x / 2)); tanh.approx has ~2^-11 relative
+// error -- below the bf16 rounding of the result, so it is used only for bf16 outputs
+__device__ __forceinline__ float silu_bf16out(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  const float hx = 0.5f * x;
+  return fmaf(hx, t, hx);
+}
 
 // load 8 consecutive elements as floats (16B for bf16, 2x16B for f32); p must be 16B aligned
 __device__ __forceinline__ void load8(const bf16* p, float* v) {

@@ -8,6 +8,7 @@
 // registers and each warp reads contiguous 16 B vectors of one token row (coalesced).
 // Deterministic: fixed-order reductions only (loopback == NCCL bitwise, graph == eager bitwise).
 #include <cstdlib>
+#include <type_traits>
 #include "../common.cuh"
 #include "../kernels.h"
 
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a,
       }
       if (a.silu) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) xv[e] = silu_f(xv[e]);
+        for (int e = 0; e < 8; ++e) xv[e] = std::is_same<TO, bf16>::value ? silu_bf16out(xv[e]) : silu_f(xv[e]);
       }
       store8(dst + (long long)t * a.out.C, xv);
     }
