@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-comm-off", action="store_true", help="N > 1: skip the COMM_OFF re-timing")
     ap.add_argument("--no-loopback", action="store_true", help="skip the n = 2/4/8 loopback projection (N = 1)")
     ap.add_argument("--kernels", default="auto", choices=["auto", "simt"])
     return ap.parse_args()
@@ -250,6 +251,31 @@ def main():
         ms = float(t.item())
     info = plan.pcpp_query()
 
+    # COMM_OFF: the same async steps with every exchange skipped; the difference is
+    # the communication the side stream failed to hide behind the compute
+    comm_off = None
+    if world > 1 and not args.no_comm_off:
+        plan.pcpp_debug_comm_off(True)
+        plan.pcpp_reset()
+        for k in range(pre):
+            plan.pcpp_step(lat, k)
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for k in range(pre, pre + args.steps):
+            plan.pcpp_step(lat, k)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_off = ev0.elapsed_time(ev1) / args.steps
+        t = torch.tensor([ms_off], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_off = float(t.item())
+        plan.pcpp_debug_comm_off(False)
+        comm_off = {"ms_per_step": round(ms_off, 4), "exposed_comm_ms": round(ms - ms_off, 4),
+                    "note": "pcpp_debug_comm_off: async steps without their NCCL exchanges (max over ranks)"}
+        _progress("COMM_OFF steps done")
+
     # per-kind breakdown of one async step, each kind captured alone (pcpp_profile)
     prof = {}
     if os.environ.get("PCPP_OP_TIMING"):          # per-op device-time table on stderr (tuning aid)
@@ -342,11 +368,25 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / 5
+            t_off = None
+            if sch == "pcpp":                      # the same steps with the exchange copies skipped
+                pl.pcpp_debug_comm_off(True)
+                pl.pcpp_reset()
+                for k in range(wv + 2):
+                    pl.pcpp_step(lat2, k)
+                torch.cuda.synchronize()
+                e0.record()
+                for k in range(wv + 2, wv + 7):
+                    pl.pcpp_step(lat2, k)
+                e1.record()
+                torch.cuda.synchronize()
+                t_off = round(e0.elapsed_time(e1) / 5, 4)
             inf2 = pl.pcpp_query()
             pl.close()
             loop[f"n{nv}" + ("" if sch == "pcpp" else "_fullmap")] = {
                               "scheme": sch, "p": pv, "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / nv, 4),
                               "projected_speedup_vs_n1": round(ms / (t / nv), 2),
+                              "ms_per_step_all_ranks_comm_off": t_off,
                               "step_flops_rank_max": inf2["step_flops_rank_max"],
                               "bytes_exchanged_per_step": sum(inf2["bytes_counted_async"])}
         loop["note"] = ("loopback: the n virtual ranks run sequentially on one GPU, exchanges are device copies; "
@@ -375,7 +415,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e, "roofline": roof, "roofline_attention": roof_attn, "cpu_baseline": cpu,
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in prof.items()},
-            "pcpp_loopback_1gpu": loop,
+            "pcpp_loopback_1gpu": loop, "comm_off": comm_off,
             "context": "paper: 2.36-8.02x speed-up on 4-8 A100-40GB, SDXL fp16 (P:5); not comparable hardware",
         }
         print(json.dumps(out), flush=True)

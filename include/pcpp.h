@@ -181,6 +181,14 @@ PCPP_API pcpp_status pcpp_query(pcpp_plan_t plan, pcpp_info* out);
  * stale -- call pcpp_reset before the next sample.  latent: as for pcpp_step. */
 typedef struct { double ms; double flops; double bytes; int launches; } pcpp_prof;
 PCPP_API pcpp_status pcpp_profile(pcpp_plan_t plan, float* latent, int kind_mask, int sync, int iters, pcpp_prof* out);
+
+/* COMM_OFF debug mode (SURVEY §8(d) "communication fully hidden"): with on != 0, asynchronous steps
+ * (k >= warmup_steps) skip every neighbour exchange -- no NCCL send/recv, no loopback copy -- and
+ * read whatever the stale buffers hold, so the step time minus the COMM_OFF step time is the
+ * exposed (non-overlapped) communication.  Warm-up steps still exchange.  The results are NOT the
+ * method's (stale data stays older than one step): timing only.  Drops cached step graphs; call
+ * between steps.  PCPP_ERR_INVALID on a NULL plan. */
+PCPP_API pcpp_status pcpp_debug_comm_off(pcpp_plan_t plan, int on);
 PCPP_API void pcpp_destroy(pcpp_plan_t plan);
 PCPP_API const char* pcpp_last_error(void);
 

@@ -382,6 +382,19 @@ pcpp_status pcpp_profile(pcpp_plan_t h, float* latent, int kind, int sync, int i
   GUARD_END
 }
 
+pcpp_status pcpp_debug_comm_off(pcpp_plan_t h, int on) {
+  GUARD_BEGIN
+  if (!h) { set_error("NULL plan"); return PCPP_ERR_INVALID; }
+  Plan& P = *h->P;
+  if (P.comm_off != (on != 0)) {
+    CKS(cudaStreamSynchronize(P.s0));
+    for (auto& g : P.graphs) for (auto& x : g) if (x) { cudaGraphExecDestroy(x); x = nullptr; }
+    P.comm_off = on != 0;
+  }
+  return PCPP_OK;
+  GUARD_END
+}
+
 void pcpp_destroy(pcpp_plan_t h) {
   if (!h) return;
   if (h->P && h->P->s0) cudaStreamSynchronize(h->P->s0);

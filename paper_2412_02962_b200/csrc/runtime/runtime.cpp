@@ -408,7 +408,8 @@ pcpp_status plan_init_comm(Plan& P) {
 
 static pcpp_status exchange(Plan& P, int xo, int sync, int par) {
   const XGroup& G = P.xg[sync][par][xo];
-  if (P.loopback && P.xasync) {      // the NCCL protocol with device copies (test mode)
+  if (P.comm_off && !sync) return PCPP_OK;
+  if (P.loopback && P.xasync) {     // the NCCL protocol with device copies (test mode)
     const auto& sr = P.seg_remote[sync][par][xo];
     CK(cudaEventRecord(P.ev_x, P.s0));
     CK(cudaStreamWaitEvent(P.s1, P.ev_x, 0));

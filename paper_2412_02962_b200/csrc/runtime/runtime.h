@@ -81,6 +81,7 @@ struct Plan {
   // NCCL backend's event protocol (one step of slack), optionally behind a per-exchange spin of
   // PCPP_XCH_DELAY x (1..5) k-cycles (delay injection: the results must not change)
   bool xasync = false; long long xdelay = 0;
+  bool comm_off = false;             // pcpp_debug_comm_off: async steps skip their exchanges
   bool use_tc = false;
 
   // program

@@ -61,7 +61,7 @@ class pcpp_prof(C.Structure):
 
 SYMBOLS = ["pcpp_plan_schedule", "pcpp_profile", "pcpp_config_default", "pcpp_get_unique_id", "pcpp_weights_len", "pcpp_manifest_count",
            "pcpp_manifest_entry", "pcpp_plan", "pcpp_plan_info", "pcpp_set_cond", "pcpp_step",
-           "pcpp_sample", "pcpp_reset", "pcpp_query", "pcpp_destroy", "pcpp_last_error",
+           "pcpp_sample", "pcpp_reset", "pcpp_query", "pcpp_debug_comm_off", "pcpp_destroy", "pcpp_last_error",
            "pcpp_op_conv", "pcpp_op_attention", "pcpp_op_groupnorm", "pcpp_op_pack_rows",
            "pcpp_op_cfg_ddim"]
 
@@ -93,6 +93,7 @@ def lib():
     L.pcpp_plan_schedule.argtypes = [I, I, I, I, D, I, C.POINTER(pcpp_config), I, C.POINTER(C.c_int), I]
     L.pcpp_plan_schedule.restype = I
     L.pcpp_profile.argtypes = [P, V, I, I, I, C.POINTER(pcpp_prof)]; L.pcpp_profile.restype = I
+    L.pcpp_debug_comm_off.argtypes = [P, I]; L.pcpp_debug_comm_off.restype = I
     L.pcpp_last_error.argtypes = []; L.pcpp_last_error.restype = C.c_char_p
     L.pcpp_op_conv.argtypes = [V, I, I, I, I, I, I, V, V, V, V, V, I, I, I, V]; L.pcpp_op_conv.restype = I
     L.pcpp_op_attention.argtypes = [V, C.POINTER(C.c_void_p), C.POINTER(C.c_int), I, I, I, I, I, V, I, I, V]
@@ -239,6 +240,10 @@ class Plan:
         pr = pcpp_prof()
         _chk(lib().pcpp_profile(self.h, _ptr(latent), kind_mask, sync, iters, C.byref(pr)), "pcpp_profile")
         return dict(ms=pr.ms, flops=pr.flops, bytes=pr.bytes, launches=pr.launches)
+
+    def pcpp_debug_comm_off(self, on: bool = True):
+        """COMM_OFF timing mode: asynchronous steps skip their exchanges (results not the method's)."""
+        _chk(lib().pcpp_debug_comm_off(self.h, 1 if on else 0), "pcpp_debug_comm_off")
 
     def close(self):
         if self.h:

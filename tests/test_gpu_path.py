@@ -238,3 +238,36 @@ def test_async_exchange_protocol_bitwise(cuda_ok, case, delay):
         del os.environ["PCPP_XCH_DELAY"]
     for k, (a, b) in enumerate(zip(got, ref)):
         assert np.array_equal(a, b), k
+
+
+@pytest.mark.gpu
+def test_comm_off_debug_mode(cuda_ok):
+    """SURVEY §8(d) COMM_OFF: warm-up steps are unchanged, async steps skip the exchange (so the
+    trajectory departs from the method's -- proving the switch removes the transfers), and switching
+    it back off after a reset restores the method's trajectory bitwise."""
+    import torch
+    model, H, n, p, w, S = "tiny", 32, 4, 0.5, 1, 4
+    ref, _ = lib_run(model, H, n, p, w, S, "fp32", "pcpp", 4)
+    cfg = pcpp.make_config(model=model, num_steps=S, precision="fp32", scheme="pcpp")
+    plan = pcpp.Plan(H, H, 4, n, p, w, cfg, weights(model, "fp32"))
+    plan.pcpp_set_cond(_data.cond(model))
+
+    def traj():
+        lat = torch.from_numpy(np.array(_data.latent(H, H))).cuda()
+        plan.pcpp_reset()
+        xs = []
+        for k in range(4):
+            plan.pcpp_step(lat, k)
+            torch.cuda.synchronize()
+            xs.append(lat.cpu().numpy().copy())
+        return xs
+
+    plan.pcpp_debug_comm_off(True)
+    off = traj()
+    plan.pcpp_debug_comm_off(False)
+    back = traj()
+    plan.close()
+    assert np.array_equal(off[0], ref[0])                # warm-up step still exchanges
+    assert not np.array_equal(off[2], ref[2])            # async steps read older stale bands
+    for k in range(4):
+        assert np.array_equal(back[k], ref[k]), k
