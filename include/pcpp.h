@@ -107,6 +107,10 @@ typedef struct {
   double step_flops;                    /* algorithmic flops of one async step (conv/GEMM 2MNK + attention
                                            4 q kv C B), summed over the ranks this plan holds */
   double step_flops_rank_max;           /* the same for the busiest single rank (interior) */
+  long long arena_bytes_per_rank;       /* activation tensors of one rank after the liveness-based memory
+                                           plan (tensors with disjoint live ranges within a step share
+                                           memory; parity-buffered / exchanged / halo tensors pinned) */
+  long long arena_bytes_unplanned;      /* the same with every tensor in its own range */
 } pcpp_info;
 
 /* ---- setup ------------------------------------------------------------------------------- */

@@ -91,6 +91,14 @@ static void fill_info(Plan& P, pcpp_info* info) {
   info->n_conv = 0; info->n_gn = (int)P.gns.size(); info->n_attn = (int)P.attns.size();
   for (const Op& o : P.ops) if (o.k == OP_CONV || o.k == OP_CONVOUT) info->n_conv++;
   info->h_latent = P.H / P.n;
+  // activation bytes of one rank arena after the memory plan, and without it (every tensor its own range)
+  if (!P.arena_tensor_bytes) plan_memory(P);
+  info->arena_bytes_per_rank = (long long)P.arena_tensor_bytes;
+  {
+    long long unplanned = 0;
+    for (const TDesc& d : P.td) unplanned += (long long)((d.bytes + 255) & ~size_t(255)) * (d.dbl ? 2 : 1);
+    info->arena_bytes_unplanned = unplanned;
+  }
   for (size_t a = 0; a < P.attns.size() && a < PCPP_MAX_LAYERS; ++a) { info->attn_h[a] = P.attns[a].h; info->attn_r[a] = P.attns[a].r; }
   // closed forms: summed over receiving ranks, one step
   const long long n = P.n, es = (long long)dtype_size(P.dtype);

@@ -8,6 +8,7 @@
 // ("issued one step ahead") and nothing waits on it inside the step.  Warm-up (sync) steps
 // exchange this step's data and wait for it ("synchronous AllGather").
 #include <algorithm>
+#include <stdexcept>
 #include <cmath>
 #include <cstring>
 #include <dlfcn.h>
@@ -54,12 +55,67 @@ Plan::~Plan() {
 // ---------------------------------------------------------------------------------------------
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-pcpp_status plan_allocate(Plan& P) {
-  size_t off = 0;
-  for (auto& t : P.td) {
-    t.off[0] = off; off = align256(off + t.bytes);
-    if (t.dbl) { t.off[1] = off; off = align256(off + t.bytes); } else t.off[1] = t.off[0];
+// Rank-arena memory plan.  Pinned tensors (one buffer per step parity, halo-padded, or read by an
+// exchange: their rows outlive the op that consumes them) get their own ranges.  Every other tensor
+// lives from the op that first touches it to the op that last reads it within one step (ops run in
+// order on the compute stream, and every kernel orders its global accesses after the previous
+// kernel's completion -- stream order, or griddepcontrol.wait under PDL), so tensors whose live
+// intervals are disjoint share memory: greedy first fit, largest first.  PCPP_MEMPLAN=0 disables it.
+size_t plan_memory(Plan& P) {
+  const int nt = (int)P.td.size();
+  std::vector<int> first(nt, 1 << 30), last(nt, -1);
+  for (int i = 0; i < (int)P.ops.size(); ++i) {
+    const Op& o = P.ops[i];
+    for (int r : {o.in0, o.in1, o.out, o.out2, o.res})
+      if (r >= 0) { first[r] = std::min(first[r], i); last[r] = std::max(last[r], i); }
   }
+  std::vector<char> pinned(nt, 0);
+  static const int plan_env = getenv("PCPP_MEMPLAN") ? atoi(getenv("PCPP_MEMPLAN")) : 1;
+  for (int t = 0; t < nt; ++t) pinned[t] = !plan_env || P.td[t].dbl || P.td[t].pad || last[t] < 0;
+  for (const HaloX& h : P.halos) pinned[h.t] = 1;
+  for (const AttnX& a : P.attns) pinned[a.kv] = 1;
+  size_t off = 0;
+  for (int t = 0; t < nt; ++t) {
+    if (!pinned[t]) continue;
+    TDesc& d = P.td[t];
+    d.off[0] = off; off = align256(off + d.bytes);
+    if (d.dbl) { d.off[1] = off; off = align256(off + d.bytes); } else d.off[1] = d.off[0];
+  }
+  const size_t base = off;
+  std::vector<int> order;
+  for (int t = 0; t < nt; ++t) if (!pinned[t]) order.push_back(t);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return P.td[a].bytes > P.td[b].bytes; });
+  std::vector<int> placed;
+  size_t top = base;
+  for (int t : order) {
+    const size_t sz = align256(P.td[t].bytes);
+    std::vector<std::pair<size_t, size_t>> busy;   // address ranges of time-overlapping placed tensors
+    for (int u : placed)
+      if (!(last[u] < first[t] || last[t] < first[u])) busy.push_back({P.td[u].off[0], P.td[u].off[0] + align256(P.td[u].bytes)});
+    std::sort(busy.begin(), busy.end());
+    size_t at = base;
+    for (auto& r : busy) {
+      if (at + sz <= r.first) break;
+      at = std::max(at, r.second);
+    }
+    P.td[t].off[0] = P.td[t].off[1] = at;
+    top = std::max(top, at + sz);
+    placed.push_back(t);
+  }
+  // invariant: no two tensors that are live at the same op share an address
+  for (size_t i = 0; i < placed.size(); ++i)
+    for (size_t j = i + 1; j < placed.size(); ++j) {
+      const int a = placed[i], b = placed[j];
+      if (last[a] < first[b] || last[b] < first[a]) continue;
+      const size_t a0 = P.td[a].off[0], a1 = a0 + P.td[a].bytes, b0 = P.td[b].off[0], b1 = b0 + P.td[b].bytes;
+      if (a0 < b1 && b0 < a1) throw std::logic_error("memory plan overlap");
+    }
+  P.arena_tensor_bytes = top;
+  return top;
+}
+
+pcpp_status plan_allocate(Plan& P) {
+  size_t off = align256(plan_memory(P));
   const size_t mb = (size_t)B_CFG * GN_G * 2 * sizeof(double);
   for (auto& g : P.gns) {
     for (int q = 0; q < 2; ++q) { g.off_m[q] = off; off = align256(off + mb); }

@@ -81,7 +81,8 @@ struct Plan {
   // NCCL backend's event protocol (one step of slack), optionally behind a per-exchange spin of
   // PCPP_XCH_DELAY x (1..5) k-cycles (delay injection: the results must not change)
   bool xasync = false; long long xdelay = 0;
-  bool comm_off = false;             // pcpp_debug_comm_off: async steps skip their exchanges
+  bool comm_off = false;
+  size_t arena_tensor_bytes = 0;     // activation part of the rank arena after the memory plan             // pcpp_debug_comm_off: async steps skip their exchanges
   bool use_tc = false;
 
   // program
@@ -144,6 +145,7 @@ struct Plan {
 pcpp_status build_program(Plan& P, int model);
 pcpp_status validate(int H, int W, int C, int n, double p, int w, const pcpp_config* cfg);
 void compute_ledgers(Plan& P, pcpp_info* info);
+size_t plan_memory(Plan& P);
 pcpp_status plan_allocate(Plan& P);
 pcpp_status plan_upload_weights(Plan& P, const float* blob);
 pcpp_status plan_build_exchanges(Plan& P);

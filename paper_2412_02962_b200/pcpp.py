@@ -41,7 +41,8 @@ class pcpp_info(C.Structure):
                 ("bytes_fullmap", C.c_longlong * 3), ("bytes_counted_async", C.c_longlong * 3),
                 ("bytes_counted_warmup", C.c_longlong * 3), ("last_step_ms", C.c_double),
                 ("device_bytes", C.c_longlong), ("n_kernels_per_step", C.c_int), ("graphs", C.c_int),
-                ("tc_kernels", C.c_int), ("step_flops", C.c_double), ("step_flops_rank_max", C.c_double)]
+                ("tc_kernels", C.c_int), ("step_flops", C.c_double), ("step_flops_rank_max", C.c_double),
+                ("arena_bytes_per_rank", C.c_longlong), ("arena_bytes_unplanned", C.c_longlong)]
 
     def as_dict(self):
         d = {}

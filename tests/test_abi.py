@@ -104,3 +104,16 @@ def test_scheduler_validation():
     with pytest.raises(pcpp.PcppError):
         info = pcpp.pcpp_plan_info(32, 32, 4, 2, 0.25, 1, cfg)
     assert info is None
+
+
+@pytest.mark.parametrize("model,H,n,prec", [("sdxl", 128, 1, "bf16"), ("sdxl", 128, 8, "bf16"), ("sdxl", 480, 8, "fp32"),
+                                           ("sdxl", 32, 2, "fp32"), ("tiny", 32, 2, "bf16"), ("tiny", 32, 4, "fp32")])
+def test_arena_memory_plan(model, H, n, prec):
+    """The liveness-based rank-arena plan (runtime.cpp plan_memory) runs host-only inside
+    pcpp_plan_info, checks its own no-overlap invariant for every pair of tensors live at the same
+    op (an overlap would fail the call), and shrinks the activation arena."""
+    cfg = pcpp.make_config(model=model, precision=prec)
+    info = pcpp.pcpp_plan_info(H, H, 4, n, 0.8 if n > 1 else 0.0, 1 if n > 1 else 0, cfg)
+    assert 0 < info["arena_bytes_per_rank"] <= info["arena_bytes_unplanned"]
+    if model == "sdxl":
+        assert info["arena_bytes_per_rank"] < 0.75 * info["arena_bytes_unplanned"]

@@ -127,3 +127,37 @@ def test_bench_workload_bf16_matches_fp32_path(cuda_ok, n):
         plan.close()
     err = float(np.linalg.norm(outs["bf16"] - outs["fp32"]) / np.linalg.norm(outs["fp32"]))
     assert err <= 2e-2, err
+
+
+@pytest.mark.parametrize("geo", [(256, 4, 0.8, "fp32"), (480, 8, 0.8, "bf16")], ids=["X2-2048px-n4", "X3-3840px-n8"])
+def test_large_resolution_tc_matches_simt_path(cuda_ok, geo):
+    """SURVEY §8(d) X2 / X3 geometries (256^2 and 480^2 latents, the paper's 2048^2 / 3840^2 images) in
+    the loopback backend (all n ranks on this GPU): the warm-up step (full-map attention over 16k /
+    57.6k tokens per head) and one async step with stale bands, tcgen05 bf16 path vs the SIMT path
+    (fp32 at X2; bf16 storage at X3, where 8 fp32 rank arenas exceed one GPU's HBM).  Exercises
+    > 2^31-byte activation offsets, thousands of GEMM / attention tiles and the arena memory plan."""
+    import torch
+    H, n, p, ref_prec = geo
+    blob = inputs.make_weight_blob(inputs.init_specs(pcpp.manifest("sdxl")))
+    xT = np.array(inputs.make_latent(H, H), dtype=np.float32)
+    cond = inputs.make_cond(1280)
+    outs = {}
+    for key, prec, kern in (("tc", "bf16", "auto"), ("simt", ref_prec, "simt")):
+        cfg = pcpp.make_config(model="sdxl", num_steps=50, precision=prec, kernels=kern)
+        plan = pcpp.Plan(H, H, 4, n, p, 1, cfg, blob)
+        plan.pcpp_set_cond(cond)
+        lat = torch.from_numpy(xT.copy()).cuda()
+        xs = []
+        for k in range(2):
+            plan.pcpp_step(lat, k)
+            torch.cuda.synchronize()
+            xs.append(lat.cpu().numpy().astype(np.float64))
+        outs[key] = xs
+        plan.close()
+        del lat
+        torch.cuda.empty_cache()
+    for k in range(2):
+        a, b = outs["tc"][k], outs["simt"][k]
+        assert np.isfinite(a).all(), k
+        err = float(np.linalg.norm(a - b) / np.linalg.norm(b))
+        assert err <= 2e-2, (k, err)
