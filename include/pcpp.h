@@ -199,7 +199,9 @@ PCPP_API const char* pcpp_last_error(void);
 /* ---- kernel-level entry points (testing / benchmarking one hot op through the ABI) -----------
  * All pointers DEVICE, layouts [rows][B][W][C] (C innermost); dtype PCPP_FP32 or PCPP_BF16 for
  * activations; enqueued on `stream` (cudaStream_t, NULL = default).  Return PCPP_ERR_INVALID on
- * unsupported shapes. */
+ * unsupported shapes, PCPP_ERR_OOM if a workspace cannot be allocated.  They share one library
+ * workspace per device and purpose (split-K / split-KV / GroupNorm partials): do not call them
+ * concurrently from several host threads or streams. */
 
 /* conv3x3 (pad 1, stride 1|2) or 1x1 GEMM (taps = 1).  x: [rows_in + 2][B][W_in][Cin] when taps = 9
  * (row 0 and row rows_in+1 are the halo rows), [rows_in][B][W_in][Cin] when taps = 1.

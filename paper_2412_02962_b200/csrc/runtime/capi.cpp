@@ -413,6 +413,27 @@ void pcpp_destroy(pcpp_plan_t h) {
   delete h;
 }
 
+// Workspaces of the kernel-level entry points: one per (device, purpose), grown on demand (the old
+// buffer is freed with cudaFree, which waits for work still using it).  Calls on several host
+// threads / streams at once would share them: the entry points are a test and benchmark surface.
+enum { WS_CONV = 0, WS_ATTN = 1, WS_GN = 2, WS_SEG = 3, WS_COEF = 4 };
+static void* op_scratch(int slot, size_t bytes, bool zero) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, std::pair<void*, size_t>> pool;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& e = pool[{dev, slot}];
+  if (bytes > e.second) {
+    if (e.first) cudaFree(e.first);
+    e = {nullptr, 0};
+    if (cudaMalloc(&e.first, bytes) != cudaSuccess) { e.first = nullptr; return nullptr; }
+    if (zero && cudaMemset(e.first, 0, bytes) != cudaSuccess) return nullptr;
+    e.second = bytes;
+  }
+  return e.first;
+}
+
 // ---- kernel-level entry points ------------------------------------------------------------------
 pcpp_status pcpp_op_conv(const void* x, int rows_in, int B, int W_in, int Cin, int taps, int stride,
                          const void* w, const float* bias, const float* temb, const void* res, void* y,
@@ -434,14 +455,9 @@ pcpp_status pcpp_op_conv(const void* x, int rows_in, int B, int W_in, int Cin, i
   g.w = w; g.wdtype = dt; g.N = Cout; g.bias = bias; g.temb = temb; g.temb_ld = Cout;
   g.out.base = y; g.out.rows = g.rows_out; g.out.B = B; g.out.W = g.w_out; g.out.C = Cout; g.out.dtype = dt;
   if (res) { g.res = g.out; g.res.base = const_cast<void*>(res); }
-  static float* ws = nullptr; static size_t ws_cap = 0;
-  const size_t need = 8ull * g.rows_out * B * g.w_out * Cout;
-  if (dt == DT_BF16 && need > ws_cap) {
-    if (ws) cudaFree(ws);
-    ws = nullptr; ws_cap = 0;
-    if (cudaMalloc(&ws, need * 4) == cudaSuccess) ws_cap = need;
-  }
-  g.ws = ws; g.ws_elems = ws_cap;
+  const size_t need = 8ull * g.rows_out * B * g.w_out * Cout;     // split-K partials (fp32)
+  float* ws = dt == DT_BF16 ? reinterpret_cast<float*>(op_scratch(WS_CONV, need * 4, false)) : nullptr;
+  g.ws = ws; g.ws_elems = ws ? need : 0;
   launch_gemm_auto(g, impl == PCPP_KERNELS_AUTO, reinterpret_cast<cudaStream_t>(stream));
   CKS(cudaGetLastError());
   return PCPP_OK;
@@ -459,25 +475,13 @@ pcpp_status pcpp_op_attention(const void* q, const void* const* kv, const int* k
   a.q = q; a.h = h; a.B = B; a.W = W; a.C = C; a.out = out; a.dtype = dtype == PCPP_FP32 ? DT_F32 : DT_BF16;
   a.nsrc = nsrc;
   for (int i = 0; i < nsrc; ++i) { a.src[i].kv = kv[i]; a.src[i].rows = kv_rows[i]; }
-  static float* ws = nullptr; static size_t ws_cap = 0;
-  const size_t need = 8ull * B * (C / 64) * h * W * 66;
-  if (a.dtype == DT_BF16 && need > ws_cap) {
-    if (ws) cudaFree(ws);
-    ws = nullptr; ws_cap = 0;
-    if (cudaMalloc(&ws, need * 4) == cudaSuccess) ws_cap = need;
-  }
-  a.ws = ws; a.ws_elems = ws_cap;
+  const size_t need = 8ull * B * (C / 64) * h * W * 66;          // split-KV partials (fp32)
+  float* ws = a.dtype == DT_BF16 ? reinterpret_cast<float*>(op_scratch(WS_ATTN, need * 4, false)) : nullptr;
+  a.ws = ws; a.ws_elems = ws ? need : 0;
   launch_attn_auto(a, impl == PCPP_KERNELS_AUTO, reinterpret_cast<cudaStream_t>(stream));
   CKS(cudaGetLastError());
   return PCPP_OK;
   GUARD_END
-}
-
-static void* scratch(size_t bytes) {
-  static void* p = nullptr; static size_t cap = 0;
-  if (bytes > cap) { if (p) cudaFree(p); p = nullptr; cap = 0; if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-                     cudaMemset(p, 0, bytes); cap = bytes; }
-  return p;
 }
 
 pcpp_status pcpp_op_groupnorm(const void* x, int rows, int B, int W, int C, const float* gamma, const float* beta,
@@ -492,7 +496,7 @@ pcpp_status pcpp_op_groupnorm(const void* x, int rows, int B, int W, int C, cons
   GnStatsArgs a;
   a.x0.base = const_cast<void*>(x); a.x0.rows = rows; a.x0.B = B; a.x0.W = W; a.x0.C = C; a.x0.dtype = dt;
   a.c0 = C; a.C = C; a.nchunk = gn_stats_chunks(rows, W);
-  char* sc = reinterpret_cast<char*>(scratch((size_t)B * a.nchunk * 32 * 2 * 8 + 256));
+  char* sc = reinterpret_cast<char*>(op_scratch(WS_GN, (size_t)B * a.nchunk * 32 * 2 * 8 + 256, true));
   if (!sc) { set_error("scratch alloc"); return PCPP_ERR_OOM; }
   a.counter = reinterpret_cast<unsigned*>(sc); a.partial = reinterpret_cast<double*>(sc + 256);
   a.m_out = m_out;
@@ -512,8 +516,8 @@ pcpp_status pcpp_op_pack_rows(const void* src, long long row_bytes, int r0, int 
   if (!src || !dst || row_bytes <= 0 || row_bytes % 16 || r0 < 0 || nrows < 0) { set_error("pcpp_op_pack_rows: bad arguments"); return PCPP_ERR_INVALID; }
   if (nrows == 0) return PCPP_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  static CopySeg* dseg = nullptr;
-  if (!dseg) CKS(cudaMalloc(&dseg, sizeof(CopySeg)));
+  CopySeg* dseg = reinterpret_cast<CopySeg*>(op_scratch(WS_SEG, sizeof(CopySeg), false));
+  if (!dseg) { set_error("scratch alloc"); return PCPP_ERR_OOM; }
   CopySeg h{reinterpret_cast<const char*>(src) + (size_t)r0 * row_bytes, dst, (unsigned long long)row_bytes * nrows};
   CKS(cudaMemcpyAsync(dseg, &h, sizeof h, cudaMemcpyHostToDevice, s));
   CKS(cudaStreamSynchronize(s));
@@ -533,8 +537,8 @@ pcpp_status pcpp_op_cfg_ddim(const float* eps, float* latent, int h, int W, floa
   const int ratio = 1000 / S, tau = (S - 1 - k) * ratio + 1, prev = tau - ratio;
   const double at = ab[tau], ap = prev >= 0 ? ab[prev] : ab[0];
   struct { double c[4]; int k; int pad[3]; } hb = {{std::sqrt(at), std::sqrt(1 - at), std::sqrt(ap), std::sqrt(1 - ap)}, 0, {0, 0, 0}};
-  static char* d = nullptr;
-  if (!d) CKS(cudaMalloc(&d, sizeof hb));
+  char* d = reinterpret_cast<char*>(op_scratch(WS_COEF, sizeof hb, false));
+  if (!d) { set_error("scratch alloc"); return PCPP_ERR_OOM; }
   CKS(cudaMemcpyAsync(d, &hb, sizeof hb, cudaMemcpyHostToDevice, s));
   CKS(cudaStreamSynchronize(s));
   launch_cfg_ddim(eps, latent, h, W, guidance, reinterpret_cast<const double*>(d), reinterpret_cast<const int*>(d + 32), s);
