@@ -110,6 +110,9 @@ void launch_temb(const float* w1, const float* b1, const float* w2, const float*
                  float* hid /*[T]*/, float* emb /*[2][T]*/, cudaStream_t s);
 void launch_temb_proj(const float* wt /*[J][T]*/, const float* bt, const float* emb, int T, int J,
                       float* out /*[2][J]*/, cudaStream_t s);
+void launch_temb_proj_multi(const float* wt, const float* bt, const float* emb, int T, int J, int nb, float* out,
+                            cudaStream_t s);
+void launch_temb_select(const float* all, const int* k_dev, int n, float* out, cudaStream_t s);
 
 // pack / unpack / loopback exchange: many contiguous 16-byte-multiple segments in one launch
 struct CopySeg { const void* src; void* dst; unsigned long long bytes; };

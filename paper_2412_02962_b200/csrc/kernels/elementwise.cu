@@ -1,3 +1,4 @@
+#include <algorithm>
 // HBM-/launch-bound elementwise kernels of the step: latent prep, nearest upsample, the fused
 // CFG (Eq. 2) + DDIM update, the timestep embedding, and the pack/unpack
 // segment copier used for band staging and the loopback exchange.
@@ -248,6 +249,48 @@ __global__ void temb_proj_kernel(const float* __restrict__ wt, const float* __re
 }
 void launch_temb_proj(const float* wt, const float* bt, const float* emb, int T, int J, float* out, cudaStream_t s) {
   launch_pdl(temb_proj_kernel, dim3((J + 7) / 8), dim3(256), 2 * T * sizeof(float), s, wt, bt, emb, T, J, out);
+}
+
+// All S steps' temb projections at once (plan / set_cond time): nb <= 8 embedding vectors per pass,
+// so the [J][T] matrix is read once per 4 steps instead of once per step.  Same per-vector
+// arithmetic and summation order as temb_proj_kernel.  out[v][J], emb[v][T].
+__global__ void temb_proj_multi_kernel(const float* __restrict__ wt, const float* __restrict__ bt,
+                                       const float* __restrict__ emb, int T, int J, int nb, float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ float se[];
+  for (int i = threadIdx.x; i < nb * T; i += blockDim.x) { const float y = emb[i]; se[i] = y / (1.f + expf(-y)); }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= J) return;
+  float a[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) a[v] = 0.f;
+  for (int i = lane; i < T; i += 32) {
+    const float wv = wt[(long long)row * T + i];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) if (v < nb) a[v] = fmaf(wv, se[v * T + i], a[v]);
+  }
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    if (v >= nb) break;
+    for (int d = 16; d > 0; d >>= 1) a[v] += __shfl_xor_sync(0xffffffffu, a[v], d);
+    if (lane == 0) out[(long long)v * J + row] = a[v] + bt[row];
+  }
+}
+void launch_temb_proj_multi(const float* wt, const float* bt, const float* emb, int T, int J, int nb, float* out, cudaStream_t s) {
+  launch_pdl(temb_proj_multi_kernel, dim3((J + 7) / 8), dim3(256), (size_t)nb * T * sizeof(float), s, wt, bt, emb, T, J, nb, out);
+}
+// per step: tproj <- tproj_all[k] (k = the device step counter)
+__global__ void temb_select_kernel(const float* __restrict__ all, const int* __restrict__ k_dev, int n, float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const float* src = all + (long long)(*k_dev) * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[i];
+}
+void launch_temb_select(const float* all, const int* k_dev, int n, float* out, cudaStream_t s) {
+  launch_pdl(temb_select_kernel, dim3((unsigned)std::min(148, (n + 255) / 256)), dim3(256), 0, s, all, k_dev, n, out);
 }
 
 // ---- segment copier: pack / unpack / loopback exchange ------------------------------------------

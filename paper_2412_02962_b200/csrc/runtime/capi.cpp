@@ -125,7 +125,7 @@ static void fill_info(Plan& P, pcpp_info* info) {
   long long nk = 0;
   for (const Op& o : P.ops) {
     switch (o.k) {
-      case OP_TEMB: nk += 3; break;
+      case OP_TEMB: nk += 1; break;
       case OP_HALO: case OP_KVX: nk += 1; break;
       case OP_GN: nk += 2 * P.nr + (P.n > 1); break;
       case OP_END: nk += 1; break;
@@ -227,6 +227,7 @@ pcpp_status pcpp_plan(int H, int W, int C, int n, double p, int w, const pcpp_co
   CKS(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   CKS(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
   if ((st = plan_init_comm(P)) != PCPP_OK) return st;
+  if ((st = temb_precompute(P)) != PCPP_OK) return st;
   if ((st = plan_autotune(P)) != PCPP_OK) return st;
   CKS(cudaDeviceSynchronize());
   *out = h.release();
@@ -306,6 +307,8 @@ pcpp_status pcpp_set_cond(pcpp_plan_t h, const float* cond) {
   if (!h || !cond) { set_error("NULL argument"); return PCPP_ERR_INVALID; }
   Plan& P = *h->P;
   CKS(cudaMemcpyAsync(P.cond, cond, (size_t)P.T * 4, cudaMemcpyHostToDevice, P.s0));
+  pcpp_status st = temb_precompute(P);
+  if (st != PCPP_OK) return st;
   CKS(cudaStreamSynchronize(P.s0));
   return PCPP_OK;
 }

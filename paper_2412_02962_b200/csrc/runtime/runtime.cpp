@@ -177,6 +177,8 @@ pcpp_status plan_allocate(Plan& P) {
   P.tproj = (float*)galloc((size_t)2 * P.J * 4); P.cond = (float*)galloc(P.T * 4);
   P.taus = (int*)galloc(P.S * 4); P.coef = (double*)galloc(P.S * 4 * 8); P.k_dev = (int*)galloc(16);
   P.coef_dpm = (double*)galloc(P.S * 6 * 8);
+  P.tproj_all = (float*)galloc((size_t)P.S * 2 * P.J * 4); P.emb_all = (float*)galloc((size_t)8 * P.T * 4);
+  P.kseq = (int*)galloc(P.S * 4);
   P.coef_anc = (double*)galloc(P.S * 5 * 8);
   if (P.cfg.scheduler == PCPP_SCHED_DPMPP2M) P.x0_hist = (float*)galloc((size_t)P.nr * (P.H / P.n) * P.W * 4 * 4);
   if (P.dtype == DT_BF16) {       // split-K workspace: up to 8 fp32 partial copies of the largest GEMM output
@@ -243,6 +245,11 @@ pcpp_status plan_allocate(Plan& P) {
   }
   CK(cudaMemcpy(P.coef_anc, ca.data(), P.S * 5 * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(P.taus, taus.data(), P.S * 4, cudaMemcpyHostToDevice));
+  {
+    std::vector<int> ks(P.S);
+    for (int k = 0; k < P.S; ++k) ks[k] = k;
+    CK(cudaMemcpy(P.kseq, ks.data(), P.S * 4, cudaMemcpyHostToDevice));
+  }
   CK(cudaMemcpy(P.coef, coef.data(), P.S * 4 * 8, cudaMemcpyHostToDevice));
   return PCPP_OK;
 }
@@ -509,6 +516,24 @@ static pcpp_status exchange(Plan& P, int xo, int sync, int par) {
 // ---------------------------------------------------------------------------------------------
 // the step
 // ---------------------------------------------------------------------------------------------
+// temb for all S steps (reading D19; SURVEY §8(a) a9 "precomputed for all S steps"): per step the
+// sinusoid -> Linear -> SiLU -> Linear (+ cond for the conditional branch), then the ResBlock
+// projections of 4 steps (8 embedding vectors) per pass over the [J][T] matrix.  Enqueued on s0;
+// called at plan time and whenever the cond vector changes.
+pcpp_status temb_precompute(Plan& P) {
+  cudaStream_t s = P.s0;
+  for (int k0 = 0; k0 < P.S; k0 += 4) {
+    const int cs = std::min(4, P.S - k0);
+    for (int kk = 0; kk < cs; ++kk)
+      launch_temb(P.wf32 + P.t_w1, P.wf32 + P.t_b1, P.wf32 + P.t_w2, P.wf32 + P.t_b2, P.cond, P.taus, P.kseq + k0 + kk,
+                  P.T, P.SIN, P.hid, P.emb_all + (size_t)kk * 2 * P.T, s);
+    launch_temb_proj_multi(P.wf32 + P.t_wt, P.wf32 + P.t_bt, P.emb_all, P.T, P.J, 2 * cs,
+                           P.tproj_all + (size_t)k0 * 2 * P.J, s);
+  }
+  CK(cudaGetLastError());
+  return PCPP_OK;
+}
+
 void launch_gemm_tc_or_simt(const Plan& P, const GemmArgs& g, cudaStream_t s);
 void launch_attn_tc_or_simt(const Plan& P, const AttnArgs& a, cudaStream_t s);
 
@@ -584,10 +609,10 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
     if (!do_op && op.k != OP_GN) continue;
     switch (op.k) {
       case OP_TEMB:
-        launch_temb(P.wf32 + P.t_w1, P.wf32 + P.t_b1, P.wf32 + P.t_w2, P.wf32 + P.t_b2, P.cond, P.taus, P.k_dev,
-                    P.T, P.SIN, P.hid, P.emb, s);
-        launch_temb_proj(P.wf32 + P.t_wt, P.wf32 + P.t_bt, P.emb, P.T, P.J, P.tproj, s);
-        P.launches_per_step += 3;
+        // the temb MLP and every ResBlock's projection depend only on (tau_k, cond): precomputed for
+        // all S steps (temb_precompute); the step selects its row by the device step counter
+        launch_temb_select(P.tproj_all, P.k_dev, 2 * P.J, P.tproj, s);
+        P.launches_per_step += 1;
         break;
       case OP_PREP: {
         const int h = P.H / n;

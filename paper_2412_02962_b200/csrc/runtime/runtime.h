@@ -113,6 +113,7 @@ struct Plan {
   void* wmat = nullptr;  float* wf32 = nullptr;
   float* emb = nullptr; float* hid = nullptr; float* tproj = nullptr; float* cond = nullptr;
   int* taus = nullptr; double* coef = nullptr; int* k_dev = nullptr;
+  float* tproj_all = nullptr; float* emb_all = nullptr; int* kseq = nullptr;   // [S][2][J] temb projections, precomputed
   double* coef_dpm = nullptr;   // DPM-Solver++(2M): [S][6] {1/alpha, sigma, sigma'/sigma, -alpha'(e^-h - 1), w0, w1}
   float* x0_hist = nullptr;     // DPM-Solver++(2M) data-prediction history, [nr][h][W][4] fp32
   double* coef_anc = nullptr;   // ancestral (eta = 1): [S][5] {sqrt(ab), sqrt(1-ab), sqrt(ab'), c_eps, sigma}
@@ -146,6 +147,7 @@ pcpp_status build_program(Plan& P, int model);
 pcpp_status validate(int H, int W, int C, int n, double p, int w, const pcpp_config* cfg);
 void compute_ledgers(Plan& P, pcpp_info* info);
 size_t plan_memory(Plan& P);
+pcpp_status temb_precompute(Plan& P);
 pcpp_status plan_allocate(Plan& P);
 pcpp_status plan_upload_weights(Plan& P, const float* blob);
 pcpp_status plan_build_exchanges(Plan& P);
