@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // SIMT implicit-GEMM conv3x3 / 1x1 (fp32 accumulate).  Used for:
 //  * every contraction in fp32 mode (parity mode, rel-L2 <= 1e-5; no fp32 tensor-core kind exists),
@@ -255,6 +256,79 @@ __global__ void __launch_bounds__(128) conv_out_bf16_kernel(const ActView in, co
   *po = make_float4(a0 + bias[0], a1 + bias[1], a2 + bias[2], a3 + bias[3]);
 }
 
+// conv_out v3 (bf16 in, Cin -> 4, fp32 out): the 9*Cin x 4 weights are staged in smem as float4 over
+// the 4 outputs, laid out [e][chunk] (chunk = tap * Cin/8 + c/8, e = channel within the 8-channel
+// chunk) so a warp's 32 lanes read 32 consecutive float4 (no bank conflicts).  A warp computes 4
+// horizontally adjacent tokens per pass (each weight read serves 4 tokens); lanes split the
+// 9*Cin/8 16-byte input chunks; the 16 partial sums are reduced with warp shuffles.
+__global__ void __launch_bounds__(256) conv_out_v3_kernel(const ActView in, const float* __restrict__ w,
+                                                          const float* __restrict__ bias, const ActView out) {
+  pdl_trigger();
+  extern __shared__ float4 wsm[];
+  const int C = in.C, K = 9 * C, nc8 = C / 8, nchunk = 9 * nc8;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {          // weights: not produced by the previous kernel
+    const int tap = i / C, cc = i - tap * C;
+    wsm[(cc & 7) * nchunk + tap * nc8 + (cc >> 3)] = make_float4(w[i], w[K + i], w[2 * K + i], w[3 * K + i]);
+  }
+  __syncthreads();
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int W = out.W, B = out.B, gpr = W / 4;
+  const long long ngroups = (long long)out.rows * B * gpr;
+  const bf16* x = reinterpret_cast<const bf16*>(in.base);
+  const float4 bv = make_float4(bias[0], bias[1], bias[2], bias[3]);
+  for (long long gi = (long long)blockIdx.x * 8 + warp; gi < ngroups; gi += (long long)gridDim.x * 8) {
+    const int w0 = (int)(gi % gpr) * 4;
+    const long long t = gi / gpr;
+    const int b = (int)(t % B), r = (int)(t / B);
+    float acc[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) acc[q][o] = 0.f;
+    for (int j = lane; j < nchunk; j += 32) {
+      const int tap = j / nc8, c = (j - tap * nc8) * 8;
+      const int dr = tap / 3 - 1, dw = tap - (tap / 3) * 3 - 1;
+      const bf16* prow = x + (((long long)(r + dr) * in.B + b) * in.W) * C + c;
+      float xv[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int wi = w0 + q + dw;
+        if (wi >= 0 && wi < in.W) load8(prow + (long long)wi * C, xv[q]);
+        else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xv[q][e] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float4 wv = wsm[e * nchunk + j];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[q][0] = fmaf(xv[q][e], wv.x, acc[q][0]); acc[q][1] = fmaf(xv[q][e], wv.y, acc[q][1]);
+          acc[q][2] = fmaf(xv[q][e], wv.z, acc[q][2]); acc[q][3] = fmaf(xv[q][e], wv.w, acc[q][3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) acc[q][o] += __shfl_xor_sync(0xffffffffu, acc[q][o], d);
+    if (lane < 4) {
+      const int q = lane;
+      float4 v;
+      v.x = acc[0][0]; v.y = acc[0][1]; v.z = acc[0][2]; v.w = acc[0][3];
+#pragma unroll
+      for (int qq = 1; qq < 4; ++qq)
+        if (q == qq) { v.x = acc[qq][0]; v.y = acc[qq][1]; v.z = acc[qq][2]; v.w = acc[qq][3]; }
+      float4* po = reinterpret_cast<float4*>(reinterpret_cast<float*>(out.base) + (((long long)r * out.B + b) * out.W + w0 + q) * 4);
+      *po = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
+    }
+  }
+}
+
 void launch_conv_out(const ActView& in, const float* w, const float* bias, const ActView& out, cudaStream_t s) {
   static const int v2 = getenv("PCPP_CONV_OUT_V2") ? atoi(getenv("PCPP_CONV_OUT_V2")) : 0;   // measured slower
   if (v2 && in.dtype == DT_BF16 && in.C % 8 == 0 && out.C == 4 && (size_t)in.C * 9 * 16 <= 160 * 1024) {
@@ -263,6 +337,13 @@ void launch_conv_out(const ActView& in, const float* w, const float* bias, const
     const int nwt = (out.W + 127) / 128;
     launch_pdl(conv_out_bf16_kernel, dim3((unsigned)(out.rows * out.B * nwt)), dim3(128), (size_t)in.C * 9 * 16, s, in, w,
                bias, out);
+    return;
+  }
+  static const int v3 = getenv("PCPP_CONV_OUT_V3") ? atoi(getenv("PCPP_CONV_OUT_V3")) : 1;
+  if (v3 && in.dtype == DT_BF16 && in.C % 8 == 0 && out.C == 4 && out.W % 4 == 0 && (size_t)in.C * 9 * 16 <= 48 * 1024) {
+    const long long ngroups = (long long)out.rows * out.B * (out.W / 4);
+    const long long blocks = std::min<long long>((ngroups + 7) / 8, 148 * 2);
+    launch_pdl(conv_out_v3_kernel, dim3((unsigned)blocks), dim3(256), (size_t)in.C * 9 * 16, s, in, w, bias, out);
     return;
   }
   const long long M = (long long)out.rows * out.B * out.W;
