@@ -8,9 +8,10 @@ Metric (BASELINE.json): per-step latency (and, across N, speed-up) of the PCPP d
 bytes exchanged per step.  One "step" = one UNet forward over both CFG branches on this rank's
 patch + the neighbour exchanges + CFG + DDIM (pcpp_step).  N = 1 is the single-device baseline
 (one patch); N > 1 splits the latent into N patches (p = 0.3 at 2, 0.8 at 4 and 8: the paper's
-Fig. 4 settings), warm-up 4.  Timed steps are post-warm-up (async) steps.
-Device time: CUDA events around K pcpp_step calls, max over ranks.  The per-step working set
-(1.57 GB of bf16 weights + activations) exceeds the 126 MB L2, so no explicit flush is needed.
+Fig. 4 settings), warm-up 4, exchanges by one-sided peer stores (PEER backend; NCCL
+with --backend nccl).  Timed steps are post-warm-up (async) steps.  Device time: CUDA events around
+K pcpp_step calls, max over ranks.  The per-step working set (1.57 GB of bf16 weights +
+activations) exceeds the 126 MB L2, so no explicit flush is needed.
 """
 from __future__ import annotations
 
@@ -27,6 +28,7 @@ sys.path.insert(0, ROOT)
 
 P_BY_N = {1: 0.0, 2: 0.3, 4: 0.8, 8: 0.8}
 METRIC = "PCPP denoising step latency (SDXL-shaped UNet, 1024x1024 / 128x128x4 latent, CFG batch 2)"
+T_START = time.time()
 
 
 def parse():
@@ -38,11 +40,15 @@ def parse():
     ap.add_argument("--res", type=int, default=128, help="latent H = W (128 -> 1024^2 image)")
     ap.add_argument("--scheme", default="pcpp", choices=["pcpp", "fullmap", "sync"])
     ap.add_argument("--p", type=float, default=None)
+    ap.add_argument("--backend", default="peer", choices=["peer", "nccl"],
+                    help="N > 1 exchange transport: one-sided peer stores (default) or NCCL send/recv")
+    ap.add_argument("--e2e-samples", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-comm-off", action="store_true", help="N > 1: skip the COMM_OFF re-timing")
-    ap.add_argument("--no-loopback", action="store_true", help="skip the n = 2/4/8 loopback projection (N = 1)")
+    ap.add_argument("--no-loopback", action="store_true", help="skip the n = 2/4/8 loopback projections (N = 1)")
+    ap.add_argument("--no-large", action="store_true", help="skip the 2048^2 / 3840^2 lines (N = 1)")
     ap.add_argument("--kernels", default="auto", choices=["auto", "simt"])
     return ap.parse_args()
 
@@ -103,37 +109,56 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons, "samples": len(self.rows)}
 
 
-def oracle_sample_ms(n, p, S, w, res_full, sample_res=32, steps=1, warmup=0, rep=None):
-    """Time the fp64 oracle (as it stands) on a bounded sample: `steps` full PCPP steps of the
-    SDXL-shaped stack at a sample_res^2 latent (same n, p, schedule), extrapolated to the
-    res_full^2 workload by the exact ratio of algorithmic flops (libpcpp's plan math)."""
-    import numpy as np
-    from oracle import model as M
-    from oracle import pcpp as OP
-    from paper_2412_02962_b200 import inputs, pcpp
-    blob = inputs.make_weight_blob(M.weight_specs("sdxl"))
-    xT = inputs.make_latent(sample_res, sample_res)
-    c = inputs.make_cond(1280)
-    cfg = OP.Config(model="sdxl", H=sample_res, W=sample_res, n=n, p=p, warmup=w, steps=S)
-    OP.sample(cfg, blob, xT, c, max_steps=warmup) if warmup else None
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        OP.sample(cfg, blob, xT, c, max_steps=1, record=False)
-        times.append(time.perf_counter() - t0)
-    pc = pcpp.make_config(model="sdxl")
-    f_full = pcpp.pcpp_plan_info(res_full, res_full, 4, n, p, w, pc)["step_flops"]
-    f_samp = pcpp.pcpp_plan_info(sample_res, sample_res, 4, n, p, w, pc)["step_flops"]
-    scale = f_full / f_samp
+# ---------------------------------------------------------------------------------------------
+# the oracle (reference / cpu_baseline) -- imports only oracle/ and the seeded generators
+# ---------------------------------------------------------------------------------------------
+def _host_info():
+    """Host threads / CPU model / BLAS of the oracle timing."""
+    cpu = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    threads, blas = os.cpu_count(), "unknown"
     try:
         from threadpoolctl import threadpool_info
-        cores = max((i.get("num_threads", 0) for i in threadpool_info()), default=os.cpu_count())
+        infos = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if infos:
+            threads = max(i.get("num_threads", 0) for i in infos)
+            blas = f"{infos[0].get('internal_api')} {infos[0].get('version')}"
     except Exception:
-        cores = os.cpu_count()
-    return times, scale, cores
+        pass
+    return threads, cpu, blas
+
+
+def oracle_step_times(n, p, S, w, res, steps):
+    """Wall time of `steps` full fp64 oracle PCPP steps (k = 0 .. steps-1; the first w synchronous) of
+    the SDXL-shaped stack at the bench's own res x res latent, n ranks simulated in one process."""
+    from oracle import model as M
+    from oracle import pcpp as OP
+    from paper_2412_02962_b200 import inputs
+    blob = inputs.make_weight_blob(M.weight_specs("sdxl"))
+    xT = inputs.make_latent(res, res)
+    c = inputs.make_cond(M.arch("sdxl")["temb"])
+    cfg = OP.Config(model="sdxl", H=res, W=res, n=n, p=p, warmup=w, steps=S)
+    times = []
+    t_prev = [time.perf_counter()]
+
+    def tick(_k):
+        t = time.perf_counter()
+        times.append(t - t_prev[0])
+        t_prev[0] = t
+    OP.sample(cfg, blob, xT, c, max_steps=steps, record=False, on_step=tick)
+    return times
 
 
 def run_reference(args):
+    """The oracle arm: the fp64 CPU oracle, as it stands, on the host cores at the bench's own
+    workload.  A full 128^2 oracle step takes about a minute, so the arm's K "steps" are a bounded
+    sample: ceil(K / 10) full steps, reported as the mean ms per full step (no extrapolation)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -141,18 +166,20 @@ def run_reference(args):
     p = P_BY_N.get(n, 0.8) if args.p is None else args.p
     w = 4 if n > 1 else 0
     S = 50
-    times, scale, cores = oracle_sample_ms(n, p, S, w, args.res, steps=args.warmup + args.steps)
-    timed = times[args.warmup:]
-    ms = 1000.0 * sum(timed) / len(timed) * scale
-    sample = (f"each step = one full fp64 oracle PCPP step (UNet fwd, both CFG branches, n={n} simulated "
-              f"ranks, CFG+DDIM) of the SDXL-shaped stack at a 32x32 latent, extrapolated x{scale:.1f} "
-              f"by the algorithmic-flop ratio to the {args.res}x{args.res} latent")
+    m = max(1, -(-args.steps // 10))
+    times = oracle_step_times(n, p, S, w, args.res, m)
+    ms = 1000.0 * sum(times) / len(times)
+    cores, cpu, blas = _host_info()
+    sample = (f"{len(times)} full fp64 oracle PCPP step(s) (UNet forward over both CFG branches, n={n} simulated "
+              f"ranks, CFG + DDIM) of the SDXL-shaped stack measured at the {args.res}x{args.res} latent itself "
+              f"(no extrapolation); per-step s: {[round(t, 2) for t in times]}")
     out = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/step", "n_gpus": n,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"sdxl-{args.res * 8} ({args.res}x{args.res}x4 latent)", "n_patches": n,
                       "cond_fraction": p, "warmup_steps": w, "num_steps": S},
-           "cpu_baseline": {"value": ms, "unit": "ms/step", "cores": cores, "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": ms, "unit": "ms/step", "cores": cores, "kind": "oracle", "sample": sample,
+                            "cpu_model": cpu, "blas": blas},
            "e2e": {"value": ms, "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -161,21 +188,23 @@ def run_reference(args):
 def _progress(msg):
     """Phase marker on stderr (the JSON line stays the only stdout line)."""
     if os.environ.get("PCPP_BENCH_QUIET") is None:
-        print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+        print(f"[bench {time.strftime('%H:%M:%S')} +{time.time() - T_START:.0f}s] {msg}", file=sys.stderr, flush=True)
 
 
 TUNE_FILE = os.path.join(ROOT, "profiles", "gemm_tune_b200.txt")
 
 
-def _comm_off_timing(plan, lat, pre, steps, ms, barrier, dist, torch):
+def _comm_off_timing(plan, lat, pre, steps, ms, dist, torch):
     """COMM_OFF re-timing at N > 1: the same async steps with every exchange skipped
-    (pcpp_debug_comm_off); step - COMM_OFF step = the communication the side stream did not hide."""
+    (pcpp_debug_comm_off); step - COMM_OFF step = the communication the overlap did not hide.
+    Every rank takes the same branch: a local failure is all-reduced before any rank returns, and the
+    plan always leaves COMM_OFF mode (finally) before anything else is measured."""
+    err, ms_off = None, 0.0
     try:
         plan.pcpp_debug_comm_off(True)
         plan.pcpp_reset()
         for k in range(pre):
             plan.pcpp_step(lat, k)
-        barrier()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
@@ -183,17 +212,65 @@ def _comm_off_timing(plan, lat, pre, steps, ms, barrier, dist, torch):
             plan.pcpp_step(lat, k)
         ev1.record()
         torch.cuda.synchronize()
-        barrier()
         ms_off = ev0.elapsed_time(ev1) / steps
-        t = torch.tensor([ms_off], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_off = float(t.item())
-        plan.pcpp_debug_comm_off(False)
-        _progress("COMM_OFF steps done")
-        return {"ms_per_step": round(ms_off, 4), "exposed_comm_ms": round(ms - ms_off, 4),
-                "note": "pcpp_debug_comm_off: async steps without their NCCL exchanges (max over ranks)"}
     except Exception as e:  # the headline line must survive a failure of this diagnostic
-        return {"error": repr(e)[:200]}
+        err = repr(e)[:200]
+    finally:
+        try:
+            plan.pcpp_debug_comm_off(False)
+        except Exception as e:
+            err = err or repr(e)[:200]
+    t = torch.tensor([ms_off, 1.0 if err else 0.0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)        # outside the try: every rank gets here
+    if t[1].item() > 0:
+        return {"error": err or "failed on another rank"}
+    ms_off = float(t[0].item())
+    _progress("COMM_OFF steps done")
+    return {"ms_per_step": round(ms_off, 4), "exposed_comm_ms": round(ms - ms_off, 4),
+            "note": "pcpp_debug_comm_off: async steps without their exchanges (max over ranks)"}
+
+
+def time_steps(plan, lat, first, count, torch):
+    """Device ms per step of pcpp_step k = first .. first+count-1 (CUDA events on the current stream,
+    which pcpp_step orders its work against)."""
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(first, first + count):
+        plan.pcpp_step(lat, k)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / count
+
+
+def loopback_line(pcpp, torch, np, inputs, res, nv, pv, scheme, S, cond, kernels, blob, comm_off=True):
+    """All n virtual ranks of an n-patch plan back to back on this GPU (LOOPBACK: exchanges are device
+    copies of exactly the bytes the transports move); ms/step of all ranks / n = the mean per-rank step
+    -- a projection of one rank on its own GPU, not a multi-GPU measurement."""
+    wv = 4 if nv > 1 else 0
+    cfg = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme=scheme, backend="loopback",
+                           kernels=kernels)
+    pl = pcpp.Plan(res, res, 4, nv, pv, wv, cfg, blob)
+    pl.pcpp_set_cond(cond)
+    lat = torch.from_numpy(np.ascontiguousarray(inputs.make_latent(res, res))).cuda()
+    pl.pcpp_reset()
+    for k in range(wv + 2):
+        pl.pcpp_step(lat, k)
+    t = time_steps(pl, lat, wv + 2, 5, torch)
+    t_off = None
+    if comm_off and nv > 1 and scheme == "pcpp":        # the same steps with the exchange copies skipped
+        pl.pcpp_debug_comm_off(True)
+        pl.pcpp_reset()
+        for k in range(wv + 2):
+            pl.pcpp_step(lat, k)
+        t_off = round(time_steps(pl, lat, wv + 2, 5, torch), 4)
+        pl.pcpp_debug_comm_off(False)
+    info = pl.pcpp_query()
+    pl.close()
+    return {"scheme": scheme, "n": nv, "p": pv, "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / nv, 4),
+            "ms_per_step_all_ranks_comm_off": t_off, "step_flops_rank_max": info["step_flops_rank_max"],
+            "bytes_exchanged_per_step": sum(info["bytes_counted_async"]),
+            "bytes_by_class": dict(zip(("attn", "conv", "gn"), info["bytes_counted_async"]))}
 
 
 def main():
@@ -203,7 +280,7 @@ def main():
         os.environ.setdefault("PCPP_TUNE_FILE", TUNE_FILE)
     import faulthandler
     # a wedged run dumps every thread's stack and exits instead of hanging the caller
-    faulthandler.dump_traceback_later(int(os.environ.get("PCPP_BENCH_WATCHDOG_S", "900")), exit=True)
+    faulthandler.dump_traceback_later(int(os.environ.get("PCPP_BENCH_WATCHDOG_S", "1500")), exit=True)
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -215,6 +292,8 @@ def main():
     N = args.gpus
     if world > 1 and world != N:
         raise SystemExit(f"WORLD_SIZE={world} but --gpus {N}")
+    if world == 1 and N > 1:
+        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -228,26 +307,46 @@ def main():
     pre = max(args.warmup, w)
     S = max(50, pre + args.steps)
 
-    nccl_id = None
-    if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(pcpp.pcpp_get_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
-
-    man = pcpp.manifest("sdxl")
-    blob = inputs.make_weight_blob(inputs.init_specs(man))
+    blob = inputs.make_weight_blob(inputs.init_specs(pcpp.manifest("sdxl")))
     cond = inputs.make_cond(1280)
     xT = inputs.make_latent(H, W)
-    cfg = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme=args.scheme,
-                           backend="nccl" if world > 1 else "loopback", rank=rank, world=max(world, 1),
-                           nccl_id=nccl_id, kernels=args.kernels)
-    plan = pcpp.Plan(H, W, 4, n if world > 1 else 1, p, w, cfg, blob) if (world > 1 or n == 1) else None
-    if plan is None:
-        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
-    del blob
-    _progress("plan built (weights uploaded, GEMMs autotuned, graphs pending)")
+
+    def make_plan(backend):
+        nccl_id = None
+        if backend == "nccl":
+            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(pcpp.pcpp_get_unique_id()), dtype=torch.uint8))
+            dist.broadcast(idt, 0)
+            nccl_id = bytes(idt.cpu().numpy().tobytes())
+        cfg = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme=args.scheme, backend=backend,
+                               rank=rank, world=max(world, 1), nccl_id=nccl_id, kernels=args.kernels)
+        pl = pcpp.Plan(H, W, 4, n, p, w, cfg, blob)
+        if backend == "peer":
+            handles = [None] * world
+            dist.all_gather_object(handles, pl.pcpp_peer_handle())
+            pl.pcpp_peer_connect(handles)
+        return pl
+
+    backend = args.backend if world > 1 else "loopback"
+    plan, backend_note, ok = None, None, 1.0
+    try:
+        plan = make_plan(backend)
+    except Exception as e:        # e.g. CUDA IPC unavailable: every rank switches to NCCL together
+        backend_note, ok = f"{backend} backend failed ({repr(e)[:160]})", 0.0
+    if world > 1:
+        t = torch.tensor([ok], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = float(t.item())
+    if ok < 1.0:
+        if world == 1 or backend == "nccl":
+            raise SystemExit(backend_note or "plan creation failed")
+        if plan is not None:
+            plan.close()
+        backend = "nccl"
+        backend_note = (backend_note or "peer backend failed on another rank") + "; fell back to nccl"
+        plan = make_plan(backend)
+    _progress(f"plan built ({backend}; weights uploaded, GEMMs autotuned, graphs pending)")
     plan.pcpp_set_cond(cond)
     patch = xT[rank * h:(rank + 1) * h] if world > 1 else xT
     lat = torch.from_numpy(np.ascontiguousarray(patch)).cuda()
@@ -279,41 +378,44 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     info = plan.pcpp_query()
+    if args.kernels == "auto" and info["simt_fallbacks"]:
+        raise SystemExit(f"{info['simt_fallbacks']} launches per step fell back to SIMT kernels")
 
     # COMM_OFF: the same async steps with every exchange skipped; the difference is
-    # the communication the side stream failed to hide behind the compute
+    # the communication the overlap failed to hide behind the compute
     comm_off = None
     if world > 1 and not args.no_comm_off:
-        comm_off = _comm_off_timing(plan, lat, pre, args.steps, ms, barrier, dist, torch)
+        comm_off = _comm_off_timing(plan, lat, pre, args.steps, ms, dist, torch)
 
-    # per-kind breakdown of one async step, each kind captured alone (pcpp_profile)
+    # per-kind breakdown of one async step, each kind captured alone (pcpp_profile; collective for
+    # the PEER backend -- every rank runs the same sequence)
     prof = {}
-    if os.environ.get("PCPP_OP_TIMING"):          # per-op device-time table on stderr (tuning aid)
+    if os.environ.get("PCPP_OP_TIMING") and world == 1:       # per-op device-time table on stderr
         plan.pcpp_profile(lat, 31, 0, 1)
     if not args.no_profile:
         for name, mask in (("conv_gemm", 1), ("attention", 2), ("groupnorm", 4), ("exchange", 8), ("other", 16)):
             prof[name] = plan.pcpp_profile(lat, mask, 0, 5)
     peaks = measured_peaks()
-    roof = None
-    roof_attn = None
+    roof = roof_attn = roof_gn = None
     if prof:
         g = prof["conv_gemm"]
         peak = peaks.get("bf16_tflops", 1590.0)
         ach = g["flops"] / (g["ms"] * 1e-3) / 1e12
         traffic, tsrc = None, None
-        tfile = os.path.join(ROOT, "profiles", "r1_gemm_traffic_step.json")
-        if os.path.exists(tfile) and args.res == 128 and world == 1 and args.scheme == "pcpp":
+        tfile = next((f for f in (os.path.join(ROOT, "profiles", f"r{r}_gemm_traffic_step.json") for r in (2, 1))
+                      if os.path.exists(f)), "")
+        if tfile and args.res == 128 and world == 1 and args.scheme == "pcpp":
             tj = json.load(open(tfile))
             traffic, tsrc = tj["gemm_dram_bytes_per_launch"], tj["source"]
-        roof = {"kernel": "gemm_tc_kernel (implicit-GEMM conv3x3 / 1x1, tcgen05) + its SIMT fallbacks",
+        roof = {"kernel": "gemm_tc_kernel / gemm_tc2_kernel (implicit-GEMM conv3x3 / 1x1, tcgen05)",
                 "bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write)",
                 "traffic_source": tsrc,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; kernel timed alone)" if peaks else "fallback",
                 "per_launch_flops": g["flops"] / max(g["launches"], 1),
                 "avg_launch_ms": g["ms"] / max(g["launches"], 1)}
-        # second kernel family: the attention is bound by exp2 on the MUFU (16/clk/SM measured,
-        # tools/ubench/mufu.cu -> 4.63e12/s at 1965 MHz), one exp2 per score = flops / (4 * 64)
+        # the attention is bound by exp2 on the MUFU (16/clk/SM measured, tools/ubench/mufu.cu ->
+        # 4.63e12/s at 1965 MHz), one exp2 per score = flops / (4 * 64)
         a = prof["attention"]
         if a["launches"]:
             ex = a["flops"] / 256.0 / (a["ms"] * 1e-3)
@@ -322,6 +424,15 @@ def main():
                          "achieved": round(ex / 1e12, 3), "peak": 4.63, "unit": "Texp2/s",
                          "frac": round(ex / 4.63e12, 4), "tensor_tflops": round(a["flops"] / (a["ms"] * 1e-3) / 1e12, 1),
                          "peak_source": "measured 16 ex2/clk/SM x 148 SMs x 1.965 GHz (profiles/r1_ubench.txt)"}
+        gn = prof["groupnorm"]
+        if gn["launches"]:
+            hbm = peaks.get("hbm_gbs", 6551.7)
+            gbs = gn["bytes"] / (gn["ms"] * 1e-3) / 1e9
+            roof_gn = {"kernel": "gn_stats / gn_finalize / gn_apply_wide (GroupNorm, fresh local + stale global)",
+                       "bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
+                       "algorithmic_bytes_per_step": gn["bytes"],
+                       "bytes_rule": "stats read of x (unless fused into the producer GEMM) + apply read x + write y",
+                       "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
     # end to end through the public API: pcpp_sample with pinned host buffers (x_T in, x_0 out)
     e2e = None
@@ -330,78 +441,75 @@ def main():
         c_h = torch.from_numpy(cond).pin_memory()
         x0_h = torch.empty((H, W, 4), dtype=torch.float32).pin_memory()
         plan.pcpp_sample_into(xT_h.data_ptr(), c_h.data_ptr(), x0_h.data_ptr())     # warm (graphs exist)
-        barrier()
-        t0 = time.perf_counter()
-        plan.pcpp_sample_into(xT_h.data_ptr(), c_h.data_ptr(), x0_h.data_ptr())
-        dt = time.perf_counter() - t0
+        dts = []
+        for _ in range(max(1, args.e2e_samples)):       # mean over samples after warm-up
+            barrier()
+            t0 = time.perf_counter()
+            plan.pcpp_sample_into(xT_h.data_ptr(), c_h.data_ptr(), x0_h.data_ptr())
+            dts.append(time.perf_counter() - t0)
+        dt = sum(dts) / len(dts)
         if dist is not None:
             t = torch.tensor([dt], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": dt * 1000.0 / S, "unit": "ms/step", "sample_ms": dt * 1000.0, "num_steps": S,
+               "samples": len(dts), "sample_ms_each": [round(x * 1000.0, 2) for x in dts],
                "h2d_bytes_per_step": (xT_h.numel() * 4 + c_h.numel() * 4) / S,
                "d2h_bytes_per_step": x0_h.numel() * 4 / S,
-               "note": "pcpp_sample: x_T/cond H2D once, S steps, x_0 D2H once; per-step = total / S"}
+               "note": "pcpp_sample (public API): x_T/cond H2D once, S steps (4 warm-up for n > 1), x_0 gathered + "
+                       "D2H once; per-step = mean sample time / S over `samples` samples after one warm sample"}
+        _progress("e2e samples done")
+    plan.close()
+    del blob
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        times, scale, cores = oracle_sample_ms(n, p, S, w, H, steps=1)
-        cpu = {"value": 1000.0 * times[0] * scale, "unit": "ms/step", "cores": cores, "kind": "oracle",
-               "sample": f"one fp64 oracle PCPP step of the SDXL-shaped stack at a 32x32 latent "
-                         f"({times[0]:.1f} s), extrapolated x{scale:.1f} by the algorithmic-flop ratio"}
+        _progress("timing the fp64 oracle (one full step at the bench latent)")
+        times = oracle_step_times(n, p, S, w, H, 1)
+        cores, cpu_model, blas = _host_info()
+        cpu = {"value": 1000.0 * times[0], "unit": "ms/step", "cores": cores, "kind": "oracle",
+               "sample": f"one full fp64 oracle PCPP step (both CFG branches, CFG + DDIM) of the SDXL-shaped "
+                         f"stack, measured at the {H}x{W} latent itself ({times[0]:.1f} s; no extrapolation)",
+               "cpu_model": cpu_model, "blas": blas}
 
-    plan.close()
-
-    # Single-GPU view of the partially conditioned path at the bench scale: all n virtual ranks of an
-    # n-patch plan run back to back on this GPU (loopback backend: exchanges are device copies of
-    # exactly the bytes NCCL would move).  ms/step of all ranks / n = the mean per-rank step (an
-    # upper bound on a rank's compute on its own GPU); a projection, not a multi-GPU measurement.
-    loop = None
-    if rank == 0 and world == 1 and not args.no_loopback and args.scheme == "pcpp" and args.res == 128:
-        loop = {}
+    # single-GPU projections (LOOPBACK, N = 1 only): the n-patch PCPP / FULLMAP steps at 1024^2, the
+    # conditioning-fraction sweep (config SW), and the 2048^2 / 3840^2 workloads (configs X2 / X3)
+    loop, sweep, large = None, None, None
+    if rank == 0 and world == 1 and args.scheme == "pcpp" and args.res == 128:
         blob2 = inputs.make_weight_blob(inputs.init_specs(pcpp.manifest("sdxl")))
-        for nv, sch in ((2, "pcpp"), (4, "pcpp"), (8, "pcpp"), (8, "fullmap")):
-            pv, wv = P_BY_N[nv], 4                 # the paper's 4 synchronous warm-up steps
-            cfg2 = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme=sch, backend="loopback",
-                                    kernels=args.kernels)
-            pl = pcpp.Plan(H, W, 4, nv, pv, wv, cfg2, blob2)
-            pl.pcpp_set_cond(cond)
-            lat2 = torch.from_numpy(np.ascontiguousarray(xT)).cuda()
-            pl.pcpp_reset()
-            for k in range(wv + 2):
-                pl.pcpp_step(lat2, k)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for k in range(wv + 2, wv + 7):
-                pl.pcpp_step(lat2, k)
-            e1.record()
-            torch.cuda.synchronize()
-            t = e0.elapsed_time(e1) / 5
-            t_off = None
-            if sch == "pcpp":                      # the same steps with the exchange copies skipped
-                pl.pcpp_debug_comm_off(True)
-                pl.pcpp_reset()
-                for k in range(wv + 2):
-                    pl.pcpp_step(lat2, k)
-                torch.cuda.synchronize()
-                e0.record()
-                for k in range(wv + 2, wv + 7):
-                    pl.pcpp_step(lat2, k)
-                e1.record()
-                torch.cuda.synchronize()
-                t_off = round(e0.elapsed_time(e1) / 5, 4)
-            inf2 = pl.pcpp_query()
-            pl.close()
-            loop[f"n{nv}" + ("" if sch == "pcpp" else "_fullmap")] = {
-                              "scheme": sch, "p": pv, "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / nv, 4),
-                              "projected_speedup_vs_n1": round(ms / (t / nv), 2),
-                              "ms_per_step_all_ranks_comm_off": t_off,
-                              "step_flops_rank_max": inf2["step_flops_rank_max"],
-                              "bytes_exchanged_per_step": sum(inf2["bytes_counted_async"])}
-        loop["note"] = ("loopback: the n virtual ranks run sequentially on one GPU, exchanges are device copies; "
-                        "ms_per_rank = all-rank time / n (a projection of one rank on its own GPU, not measured); "
-                        "n8_fullmap = the DistriFusion-style full-map exchange (P:86) on the same kernels")
+        if not args.no_loopback:
+            loop = {}
+            for nv, sch in ((2, "pcpp"), (4, "pcpp"), (8, "pcpp"), (8, "fullmap")):
+                r = loopback_line(pcpp, torch, np, inputs, H, nv, P_BY_N[nv], sch, S, cond, args.kernels, blob2)
+                r["projected_speedup_vs_n1"] = round(ms / r["ms_per_rank"], 2)
+                loop[f"n{nv}" + ("" if sch == "pcpp" else "_fullmap")] = r
+            loop["note"] = ("loopback: the n virtual ranks run sequentially on one GPU, exchanges are device copies; "
+                            "ms_per_rank = all-rank time / n (a projection of one rank on its own GPU, not measured); "
+                            "n8_fullmap = the DistriFusion-style full-map exchange (P:86) on the same kernels")
+            _progress("1024^2 loopback projections done")
+            sweep = {}
+            for pv in (0.0, 0.125, 0.25, 0.5, 1.0):       # config SW: p sweep at 1024^2, n = 8
+                r = loopback_line(pcpp, torch, np, inputs, H, 8, pv, "pcpp", S, cond, args.kernels, blob2, comm_off=False)
+                sweep[str(pv)] = {k: r[k] for k in ("ms_per_rank", "ms_per_step_all_ranks", "bytes_exchanged_per_step",
+                                                   "bytes_by_class")}
+            sweep["note"] = "config SW (n = 8 at 1024^2, loopback projection); error vs oracle: tests/test_gpu_golden.py"
+            _progress("SW sweep done")
+        if not args.no_large:
+            large = {}
+            for res, nvs in ((256, (1, 4, 8)), (480, (1, 8))):     # configs X2 / X3
+                base = None
+                for nv in nvs:
+                    schemes = ("pcpp", "fullmap") if (nv == 8 and res == 256) else ("pcpp",)
+                    for sch in schemes:
+                        r = loopback_line(pcpp, torch, np, inputs, res, nv, P_BY_N[nv], sch, S, cond, args.kernels,
+                                          blob2, comm_off=False)
+                        if nv == 1:
+                            base = r["ms_per_rank"]
+                        r["projected_speedup_vs_n1"] = round(base / r["ms_per_rank"], 2) if base else None
+                        large[f"res{res * 8}_n{nv}" + ("" if sch == "pcpp" else "_fullmap")] = r
+                _progress(f"{res * 8}^2 lines done")
+            large["note"] = ("2048^2 (X2) and 3840^2 (X3) SDXL-shaped steps: n = 1 measured on this GPU, n > 1 as loopback "
+                             "projections (ms_per_rank = all-rank time / n)")
         del blob2
 
     if rank == 0:
@@ -416,6 +524,8 @@ def main():
                        "global_batch": 2, "seq_len": H * W, "parallelism": f"pcpp-patch{n}",
                        "n_patches": n, "cond_fraction": p, "warmup_steps": w, "num_steps": S,
                        "scheme": args.scheme, "step_flops_per_rank": info["step_flops_rank_max"],
+                       "backend": ["nccl", "loopback", "peer"][info["backend"]], "backend_note": backend_note,
+                       "simt_fallbacks_per_step": info["simt_fallbacks"],
                        "l2": "per-step working set (1.57 GB bf16 weights + activations) >> 126 MB L2; no flush"},
             "bytes_exchanged_per_step": {"async": dict(zip(cls, info["bytes_counted_async"])),
                                          "warmup": dict(zip(cls, info["bytes_counted_warmup"])),
@@ -423,10 +533,12 @@ def main():
             "achieved_tflops_step": round(info["step_flops_rank_max"] / (ms * 1e-3) / 1e12, 1),
             "gpu_launches": info["n_kernels_per_step"] * args.steps,
             "clocks": clk.summary(),
-            "e2e": e2e, "roofline": roof, "roofline_attention": roof_attn, "cpu_baseline": cpu,
+            "e2e": e2e, "roofline": roof, "roofline_attention": roof_attn, "roofline_groupnorm": roof_gn,
+            "cpu_baseline": cpu,
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in prof.items()},
-            "pcpp_loopback_1gpu": loop, "comm_off": comm_off,
+            "pcpp_loopback_1gpu": loop, "sw_sweep_1024_n8": sweep, "large_resolutions": large, "comm_off": comm_off,
             "context": "paper: 2.36-8.02x speed-up on 4-8 A100-40GB, SDXL fp16 (P:5); not comparable hardware",
+            "bench_wall_s": round(time.time() - T_START, 1),
         }
         print(json.dumps(out), flush=True)
     if dist is not None:

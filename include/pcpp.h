@@ -48,8 +48,18 @@ enum { PCPP_FP32 = 0, PCPP_BF16 = 1 };                       /* precision */
 enum { PCPP_SCHEME_PCPP = 0,                                 /* stale partial bands, p2p (§3.2-3.3) */
        PCPP_SCHEME_FULLMAP = 1,                              /* DistriFusion full-map all-gather */
        PCPP_SCHEME_SYNC = 2 };                               /* every step synchronous */
-enum { PCPP_MODEL_TINY = 0, PCPP_MODEL_SDXL = 1 };           /* config T / SDXL-shaped */
-enum { PCPP_COMM_NCCL = 0, PCPP_COMM_LOOPBACK = 1 };
+enum { PCPP_MODEL_TINY = 0, PCPP_MODEL_SDXL = 1,            /* config T / SDXL-shaped */
+       PCPP_MODEL_TINY_XF = 2, PCPP_MODEL_SDXL_XF = 3 };     /* the same stacks with SDXL's full transformer
+                                                                block in every attention layer: LayerNorm,
+                                                                self-attention, LayerNorm, cross-attention to a
+                                                                77-token context, LayerNorm, GEGLU feed-forward
+                                                                (§2.1; DESIGN D25) */
+#define PCPP_CTX_LEN 77                                       /* context tokens of the _XF models (D26) */
+enum { PCPP_COMM_NCCL = 0,       /* one process per GPU; bands by grouped ncclSend/Recv on a comm stream */
+       PCPP_COMM_LOOPBACK = 1,   /* all n virtual ranks in this process on one GPU; transfers = device copies */
+       PCPP_COMM_PEER = 2 };     /* one process per GPU; bands as one-sided stores into the peers' device
+                                    memory (CUDA IPC mapping: NVLink stores across GPUs) + device flag
+                                    barriers -- see pcpp_peer_handle / pcpp_peer_connect */
 enum { PCPP_KERNELS_AUTO = 0, PCPP_KERNELS_SIMT = 1 };        /* bf16: tcgen05 kernels (AUTO) or SIMT */
 
 typedef struct pcpp_plan_s* pcpp_plan_t;                     /* opaque; owned by libpcpp */
@@ -111,6 +121,10 @@ typedef struct {
                                            plan (tensors with disjoint live ranges within a step share
                                            memory; parity-buffered / exchanged / halo tensors pinned) */
   long long arena_bytes_unplanned;      /* the same with every tensor in its own range */
+  int simt_fallbacks;                   /* launches of a captured step that asked for the tcgen05 path but ran
+                                           the SIMT kernel (unsupported shape); 0 on every SDXL/tiny shape */
+  int backend;                          /* effective PCPP_COMM_* (n == 1 always runs LOOPBACK) */
+  char comm_lib[192];                   /* NCCL backend: path of the libnccl that was loaded ("" otherwise) */
 } pcpp_info;
 
 /* ---- setup ------------------------------------------------------------------------------- */
@@ -159,6 +173,14 @@ PCPP_API int pcpp_plan_schedule(int H, int W, int C, int n_patches, double cond_
  * it to the timestep embedding (reading D11).  Copied; asynchronous on the compute stream. */
 PCPP_API pcpp_status pcpp_set_cond(pcpp_plan_t plan, const float* cond_host);
 
+/* _XF models only: set the cross-attention context (HOST fp32 [2][PCPP_CTX_LEN][ctx_dim], ctx_dim =
+ * 2048 SDXL_XF / 256 TINY_XF; [0] = the unconditional branch's context, [1] = the prompt's; reading
+ * D26).  The per-layer context keys/values (ctx W_k, ctx W_v) are computed here, once per context,
+ * by the same GEMM kernels -- the context does not change across the S steps.  Must be called before
+ * the first pcpp_step / pcpp_sample of an _XF plan (PCPP_ERR_STATE otherwise); PCPP_ERR_INVALID for
+ * the other models.  Synchronises the compute stream. */
+PCPP_API pcpp_status pcpp_set_context(pcpp_plan_t plan, const float* ctx_host);
+
 /* One denoising step k = t: UNet forward on this rank's patch for both CFG branches (batch 2),
  * the exchanges of §3.2, then CFG (Eq. 2) + DDIM on the patch, in place.
  * latent: DEVICE fp32.  NCCL: this rank's patch [h][W][C].  LOOPBACK: the full map [H][W][C].
@@ -175,6 +197,22 @@ PCPP_API pcpp_status pcpp_sample(pcpp_plan_t plan, const float* xT_host, const f
 PCPP_API pcpp_status pcpp_reset(pcpp_plan_t plan);
 
 PCPP_API pcpp_status pcpp_query(pcpp_plan_t plan, pcpp_info* out);
+
+/* ---- PEER backend (App. A: one-sided, batched signalling) ---------------------------------
+ * After pcpp_plan on every rank: each rank calls pcpp_peer_handle (64 bytes: the CUDA IPC handle of
+ * its arena), the caller all-gathers the n handles over any host transport, and each rank calls
+ * pcpp_peer_connect with the n handles concatenated in rank order.  Every rank's plan has the same
+ * arena layout, so rank i pushes a band to rank j's buffer at the same offset in j's mapping.
+ * Protocol per step k: a device barrier (all peers finished step k-1), then the pushes of step k are
+ * issued on the comm stream behind their producers and consumed at step k+1 (async steps), or on
+ * the compute stream followed by a barrier (warm-up steps).  pcpp_step, pcpp_sample, pcpp_profile
+ * (with the exchange kind) and pcpp_destroy are COLLECTIVE for this backend: every rank calls them
+ * in the same order.  A barrier that waits > 60 s traps (poisoning the plan).
+ * Errors: PCPP_ERR_STATE if the plan is not a PEER plan or is already connected; PCPP_ERR_CUDA if a
+ * handle cannot be opened.  pcpp_step before pcpp_peer_connect returns PCPP_ERR_STATE. */
+#define PCPP_PEER_HANDLE_BYTES 64
+PCPP_API pcpp_status pcpp_peer_handle(pcpp_plan_t plan, void* out64);
+PCPP_API pcpp_status pcpp_peer_connect(pcpp_plan_t plan, const void* handles);
 
 /* Per-kind device time of one step, measured in isolation: the ops of `kind_mask` (1 conv/GEMM,
  * 2 attention, 4 GroupNorm, 8 exchanges, 16 other elementwise) of a step of type `sync` are captured

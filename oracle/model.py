@@ -48,21 +48,34 @@ from .schedule import band_rows
 
 G_GROUPS = 32
 GN_EPS = 1e-5
+LN_EPS = 1e-5
 HEAD_DIM = 64
+
+
+def _erf(x):
+    from scipy.special import erf       # library primitive (the error function)
+    return erf(x)
 
 # ----------------------------------------------------------------------------
 # Architecture description
 # ----------------------------------------------------------------------------
 
 
+CTX_LEN = 77          # text tokens of the cross-attention context (SDXL's CLIP length; reading D26)
+
+
 def arch(model: str) -> dict:
-    """Channel widths / depths.  SDXL: App. A; TINY: config T."""
-    if model == "sdxl":
-        return dict(model=model, C0=320, chans=[320, 640, 1280], depth=[0, 2, 10],
-                    temb=1280, sin_dim=320, levels=3)
-    if model == "tiny":
-        return dict(model=model, C0=128, chans=[128], depth=[1], temb=512,
-                    sin_dim=128, levels=1)
+    """Channel widths / depths.  SDXL: App. A; TINY: config T.  The '_xf' variants
+     replace each attention layer of an AS stack by SDXL's full transformer block
+    (LayerNorm, self-attention, LayerNorm, cross-attention to a 77-token context, LayerNorm, GEGLU
+    feed-forward; reading D25), with a context of dimension ctx_dim (SDXL 2048)."""
+    base, xf = (model[:-3], True) if model.endswith("_xf") else (model, False)
+    if base == "sdxl":
+        return dict(model=model, base=base, xf=xf, C0=320, chans=[320, 640, 1280], depth=[0, 2, 10],
+                    temb=1280, sin_dim=320, levels=3, ctx_dim=2048)
+    if base == "tiny":
+        return dict(model=model, base=base, xf=xf, C0=128, chans=[128], depth=[1], temb=512,
+                    sin_dim=128, levels=1, ctx_dim=256)
     raise ValueError(model)
 
 
@@ -77,14 +90,23 @@ def _rb_specs(pre, cin, cout, T):
     return s
 
 
-def _as_specs(pre, C, depth):
+def _as_specs(pre, C, depth, xf=False, ctx_dim=0):
     s = [(f"{pre}.gn.g", (C,), "gamma"), (f"{pre}.gn.b", (C,), "beta"),
          (f"{pre}.proj_in.w", (C, C), "lin"), (f"{pre}.proj_in.b", (C,), "bias")]
     for d in range(depth):
         a = f"{pre}.attn{d}"
+        if xf:
+            s += [(f"{a}.ln1.g", (C,), "gamma"), (f"{a}.ln1.b", (C,), "beta")]
         s += [(f"{a}.wq", (C, C), "lin"), (f"{a}.wk", (C, C), "lin"),
               (f"{a}.wv", (C, C), "lin"), (f"{a}.wo", (C, C), f"lin_res{depth}"),
               (f"{a}.bo", (C,), "bias")]
+        if xf:   # reading D25: cross-attention (no q/k/v bias, as SDXL) and the GEGLU feed-forward
+            s += [(f"{a}.ln2.g", (C,), "gamma"), (f"{a}.ln2.b", (C,), "beta"),
+                  (f"{a}.xq", (C, C), "lin"), (f"{a}.xk", (C, ctx_dim), "lin"), (f"{a}.xv", (C, ctx_dim), "lin"),
+                  (f"{a}.xo", (C, C), f"lin_res{depth}"), (f"{a}.xbo", (C,), "bias"),
+                  (f"{a}.ln3.g", (C,), "gamma"), (f"{a}.ln3.b", (C,), "beta"),
+                  (f"{a}.ff1.w", (8 * C, C), "lin"), (f"{a}.ff1.b", (8 * C,), "bias"),
+                  (f"{a}.ff2.w", (C, 4 * C), f"lin_res{depth}"), (f"{a}.ff2.b", (C,), "bias")]
     s += [(f"{pre}.proj_out.w", (C, C), "lin_res1"), (f"{pre}.proj_out.b", (C,), "bias")]
     return s
 
@@ -98,7 +120,7 @@ def _blocks(model: str):
     a = arch(model)
     C = a["chans"]
     B = []
-    if model == "tiny":
+    if a["base"] == "tiny":
         B.append(("conv_in", "conv_in", (4, C[0])))
         for j in range(2):
             B.append(("rb", f"blk{j}.rb", (C[0], C[0])))
@@ -152,7 +174,7 @@ def manifest(model: str) -> list[tuple[str, tuple, str]]:
         elif kind == "rb":
             m += _rb_specs(pre, args[0], args[1], T)
         elif kind == "as":
-            m += _as_specs(pre, args[0], args[1])
+            m += _as_specs(pre, args[0], args[1], a["xf"], a["ctx_dim"])
         elif kind in ("down", "up"):
             c = args[0]
             m += [(f"{pre}.conv.w", (c, 3, 3, c), "conv"), (f"{pre}.conv.b", (c,), "bias")]
@@ -399,6 +421,53 @@ def attention(ctx: Ctx, hs, wq, wk, wv, wo, bo):
     return out
 
 
+def layer_norm(xs, gamma, beta):
+    """LayerNorm over the channels of every token (reading D25; eps = 1e-5, biased variance):
+    y = gamma (x - mean_c x) / sqrt(var_c x + eps) + beta.  Patch-local: no exchange."""
+    out = []
+    for x in xs:
+        mu = x.mean(axis=-1, keepdims=True)
+        var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+        out.append((x - mu) / np.sqrt(var + LN_EPS) * gamma + beta)
+    return out
+
+
+def cross_attention(hs, context, wq, wk, wv, wo, bo):
+    """Multi-head cross-attention of every token to the 77-token context (reading D25/D26):
+    Q = X W_q, K = ctx W_k, V = ctx W_v (no bias), heads = C/64, scale 1/8, O W_o + b_o.
+    context: [B=2, 77, ctx_dim] (b = 0 uncond, b = 1 cond).  Patch-local: no exchange."""
+    out = []
+    for x in hs:
+        Bn, h, W, C = x.shape
+        O = np.zeros((Bn, h * W, C))
+        for bb in range(Bn):
+            q = x[bb].reshape(h * W, C) @ wq.T
+            k = context[bb] @ wk.T
+            v = context[bb] @ wv.T
+            for hd in range(C // HEAD_DIM):
+                sl = slice(hd * HEAD_DIM, (hd + 1) * HEAD_DIM)
+                S = (q[:, sl] @ k[:, sl].T) / math.sqrt(HEAD_DIM)
+                O[bb, :, sl] = _softmax_rows(S) @ v[:, sl]
+        out.append(O.reshape(Bn, h, W, C) @ wo.T + bo)
+    return out
+
+
+def gelu(x):
+    """Exact GELU x Phi(x) = x (1 + erf(x / sqrt 2)) / 2 (SDXL's GEGLU uses the exact form; D25)."""
+    return 0.5 * x * (1.0 + _erf(x / math.sqrt(2.0)))
+
+
+def geglu_ff(xs, w1, b1, w2, b2):
+    """GEGLU feed-forward (reading D25): u = X W_1 + b_1 (8C), split into the value a (first 4C)
+    and the gate g (last 4C); FF(X) = (a * gelu(g)) W_2 + b_2."""
+    out = []
+    for x in xs:
+        u = x @ w1.T + b1
+        half = u.shape[-1] // 2
+        out.append((u[..., :half] * gelu(u[..., half:])) @ w2.T + b2)
+    return out
+
+
 def upsample2(xs):
     """Nearest x2 (SDXL Upsample2D), patch-local: low rows [i h, (i+1) h) map to
     high rows [2 i h, 2 (i+1) h)."""
@@ -435,23 +504,38 @@ def resblock(ctx, P, pre, xs, emb):
     return [a + s for a, s in zip(h, skip)]
 
 
-def attn_stack(ctx, P, pre, xs, depth):
-    """AS(C, d), App. A."""
+def attn_stack(ctx, P, pre, xs, depth, context=None):
+    """AS(C, d), App. A.  With a context (the '_xf' models) every layer is SDXL's transformer
+    block (reading D25): h += SA(LN1 h) [PCPP bands of K/V of LN1 h]; h += CA(LN2 h, ctx);
+    h += FF(LN3 h)."""
     g = group_norm(ctx, xs, P(f"{pre}.gn.g"), P(f"{pre}.gn.b"), act=False)
     h = linear(g, P(f"{pre}.proj_in.w"), P(f"{pre}.proj_in.b"))
     for d in range(depth):
         a = f"{pre}.attn{d}"
-        o = attention(ctx, h, P(f"{a}.wq"), P(f"{a}.wk"), P(f"{a}.wv"), P(f"{a}.wo"), P(f"{a}.bo"))
+        x = layer_norm(h, P(f"{a}.ln1.g"), P(f"{a}.ln1.b")) if context is not None else h
+        o = attention(ctx, x, P(f"{a}.wq"), P(f"{a}.wk"), P(f"{a}.wv"), P(f"{a}.wo"), P(f"{a}.bo"))
         h = [x + y for x, y in zip(h, o)]
+        if context is not None:
+            x = layer_norm(h, P(f"{a}.ln2.g"), P(f"{a}.ln2.b"))
+            o = cross_attention(x, context, P(f"{a}.xq"), P(f"{a}.xk"), P(f"{a}.xv"), P(f"{a}.xo"), P(f"{a}.xbo"))
+            h = [x + y for x, y in zip(h, o)]
+            x = layer_norm(h, P(f"{a}.ln3.g"), P(f"{a}.ln3.b"))
+            o = geglu_ff(x, P(f"{a}.ff1.w"), P(f"{a}.ff1.b"), P(f"{a}.ff2.w"), P(f"{a}.ff2.b"))
+            h = [x + y for x, y in zip(h, o)]
     o = linear(h, P(f"{pre}.proj_out.w"), P(f"{pre}.proj_out.b"))
     return [x + y for x, y in zip(o, xs)]
 
 
-def unet(ctx: Ctx, P: Params, model: str, latents, emb):
+def unet(ctx: Ctx, P: Params, model: str, latents, emb, context=None):
     """eps_theta over n patches, both CFG branches as batch 2 (b=0 uncond, b=1 cond).
 
-    latents: list over ranks of [h, W, 4] float64.  Returns list of [2, h, W, 4].
+    latents: list over ranks of [h, W, 4] float64.  context: [2, 77, ctx_dim] for the '_xf'
+    models (required there), else None.  Returns list of [2, h, W, 4].
     """
+    if arch(model)["xf"] != (context is not None):
+        raise ValueError("the '_xf' models need a context, the others take none")
+    if context is not None:
+        context = np.asarray(context, dtype=np.float64)
     xs = [np.stack([x, x]).astype(np.float64) for x in latents]
     skips = []
     h = None
@@ -466,7 +550,7 @@ def unet(ctx: Ctx, P: Params, model: str, latents, emb):
         elif kind == "rb":
             h = resblock(ctx, P, pre, h, emb)
         elif kind == "as":
-            h = attn_stack(ctx, P, pre, h, args[1])
+            h = attn_stack(ctx, P, pre, h, args[1], context)
         elif kind == "down":
             h = conv3x3(ctx, h, P(f"{pre}.conv.w"), P(f"{pre}.conv.b"), stride=2)
         elif kind == "up":

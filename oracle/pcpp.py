@@ -50,8 +50,9 @@ def split(x: np.ndarray, n: int):
 
 
 def sample(cfg: Config, blob: np.ndarray, x_T: np.ndarray, cond: np.ndarray,
-           record: bool = True, max_steps: int | None = None):
-    """Run the n-patch PCPP sampler.
+           record: bool = True, max_steps: int | None = None, on_step=None, context=None):
+    """Run the n-patch PCPP sampler.  on_step(k), if given, is called after step k (timing hook).
+    context: [2, 77, ctx_dim] cross-attention context of the '_xf' models (b = 0 uncond, 1 cond).
 
     Returns dict(x0=[H,W,4], xs=[x after every step], eps=[per-step eps_hat],
                  ledger=[per-step list of (kind, lid, src, dst, elems)],
@@ -69,7 +70,7 @@ def sample(cfg: Config, blob: np.ndarray, x_T: np.ndarray, cond: np.ndarray,
         mode = "sync" if sync else "async"
         ctx = M.Ctx(n, cfg.p, mode, "fullmap" if cfg.scheme == "fullmap" else "pcpp", prev)
         emb = M.timestep_embedding(P, cfg.model, taus[k], cond)
-        eps = M.unet(ctx, P, cfg.model, patches, emb)
+        eps = M.unet(ctx, P, cfg.model, patches, emb, context)
         eps_hat = [cfg_combine(e[0], e[1], cfg.guidance) for e in eps]   # b=0 uncond, b=1 cond
         if cfg.scheduler == "dpmpp2m":
             if k == 0:
@@ -84,6 +85,8 @@ def sample(cfg: Config, blob: np.ndarray, x_T: np.ndarray, cond: np.ndarray,
         else:
             patches = [ddim_step(x, e, cfg.steps, k) for x, e in zip(patches, eps_hat)]
         prev = ctx.nxt
+        if on_step is not None:
+            on_step(k)
         if record:
             out["xs"].append(np.concatenate(patches, axis=0))
             out["eps"].append(np.concatenate(eps_hat, axis=0))
@@ -93,7 +96,7 @@ def sample(cfg: Config, blob: np.ndarray, x_T: np.ndarray, cond: np.ndarray,
     return out
 
 
-def forward_pair(cfg: Config, blob, x, tau, cond, first_mode: str, second_mode: str):
+def forward_pair(cfg: Config, blob, x, tau, cond, first_mode: str, second_mode: str, context=None):
     """Two forwards on identical (x, tau): the second reads the store the first
     wrote.  Used by pin P6 (fresh-then-async must reproduce the fresh output)."""
     P = M.Params(cfg.model, blob)
@@ -101,9 +104,9 @@ def forward_pair(cfg: Config, blob, x, tau, cond, first_mode: str, second_mode: 
     emb = M.timestep_embedding(P, cfg.model, tau, cond)
     scheme = "fullmap" if cfg.scheme == "fullmap" else "pcpp"
     c1 = M.Ctx(cfg.n, cfg.p, first_mode, scheme)
-    e1 = M.unet(c1, P, cfg.model, patches, emb)
+    e1 = M.unet(c1, P, cfg.model, patches, emb, context)
     c2 = M.Ctx(cfg.n, cfg.p, second_mode, scheme, c1.nxt)
-    e2 = M.unet(c2, P, cfg.model, patches, emb)
+    e2 = M.unet(c2, P, cfg.model, patches, emb, context)
     return e1, e2
 
 

@@ -33,9 +33,9 @@ struct GemmArgs {
   ActView out, out2; int n_split = 1 << 30;  // cols >= n_split -> out2[col - n_split]
   float* ws = nullptr; size_t ws_elems = 0;  // split-K fp32 workspace (optional)
   // optional fused GroupNorm(32) statistics of `out` (tcgen05 path only): partial sums land in
-  // gn_part [slots][B=2][G=32][2] fp32 and *gn_slots (host) receives the slot count, 0 if the
+  // gn_part [slots][B=2][G=32][2] fp64 and *gn_slots (host) receives the slot count, 0 if the
   // launch did not produce them (the consumer then runs the standalone stats kernel)
-  float* gn_part = nullptr; int* gn_slots = nullptr;
+  double* gn_part = nullptr; int* gn_slots = nullptr;
 };
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 
@@ -45,7 +45,9 @@ void launch_conv_out(const ActView& in, const float* w /*[4][9*Cin] fp32*/, cons
 
 // Partially conditioned attention: Q from the local patch; K/V from up to 3 row
 // sources [top band ; local ; bottom band] each laid out [rows][B][W][2C] (K cols [0,C), V [C,2C)).
-struct AttnSrc { const void* kv = nullptr; int rows = 0; };
+// nkeys > 0: only the first nkeys keys (token order r * W + w) of the source are attended (the
+// 77-token cross-attention context, padded to whole rows); 0 = all rows * W keys.
+struct AttnSrc { const void* kv = nullptr; int rows = 0; int nkeys = 0; };
 struct AttnArgs {
   const void* q = nullptr;    // [h][B][W][C]
   AttnSrc src[3]; int nsrc = 0;
@@ -59,15 +61,14 @@ void launch_attn_simt(const AttnArgs& a, cudaStream_t s);
 // GroupNorm(32).  Stats: fresh local sums m[b][g][{sum, sumsq}] (fp64) of the rank's patch.
 struct GnStatsArgs {
   ActView x0, x1; int c0 = 0; int C = 0;
-  double* partial = nullptr;     // [B][nchunk][G][2] scratch
-  unsigned* counter = nullptr;   // zero-initialised; reset by the last CTA
+  double* partial = nullptr;     // [nchunk][2][G][2] scratch (per-CTA slots, summed by gn_finalize)
   double* m_out = nullptr;       // [B][G][2]
   int nchunk = 0;
 };
 void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s);
 // m_out[b][g][k] = sum over slots of part[slot][b][g][k] (fp64, fixed order): the finalize of the
 // GEMM-epilogue-fused statistics
-void launch_gn_finalize(const float* part, int nslots, double* m_out, cudaStream_t s);
+void launch_gn_finalize(const double* part, int nslots, double* m_out, cudaStream_t s);
 int gn_stats_chunks(int rows, int W);
 void gn_init();
 
@@ -83,8 +84,13 @@ struct GnApplyArgs {
   double count = 0;              // N = H_l W_l C/G (global)
 };
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s);
-// stats + apply in one launch (modes 0 and 2); counter must point at 2 zero-initialised words
-void launch_gn_fused(const GnStatsArgs& sa, const GnApplyArgs& aa, cudaStream_t s);
+
+// SDXL transformer block (kernels/xformer.cu; reading D25): LayerNorm of every token over its C
+// channels (false if C is unsupported); GEGLU gate out = u[:, :4C] * gelu(u[:, 4C:]); the context
+// [B][L][D] fp32 laid out as the rows of a [rows][B][W][D] key source (keys >= L zero)
+bool launch_layernorm(const ActView& x, const ActView& y, const float* gamma, const float* beta, cudaStream_t s);
+void launch_geglu(const ActView& u, const ActView& out, cudaStream_t s);
+void launch_ctx_layout(const float* ctx, const ActView& out, int L, cudaStream_t s);
 
 // latent [h][W][4] fp32 -> padded xin [h][2][W][4] fp32 (both CFG branches)
 void launch_prep_latent(const float* latent, const ActView& xin, cudaStream_t s);
@@ -117,6 +123,16 @@ void launch_temb_select(const float* all, const int* k_dev, int n, float* out, c
 // pack / unpack / loopback exchange: many contiguous 16-byte-multiple segments in one launch
 struct CopySeg { const void* src; void* dst; unsigned long long bytes; };
 void launch_copy_segments(const CopySeg* segs_dev, int nseg, unsigned long long max_bytes, cudaStream_t s);
+
+// PEER backend barrier (kernels/peer.cu): every rank publishes ++(*epoch) into remote[j] (= peer j's
+// flags[me]) and waits until flags[j] >= epoch for every peer j != me.
+struct PeerBarrier {
+  unsigned long long* epoch = nullptr;         // local counter (this rank's arena)
+  const unsigned long long* flags = nullptr;   // local [n], written by the peers
+  unsigned long long* remote[8] = {};          // peer j's flags[me] (IPC-mapped)
+  int n = 1, me = 0;
+};
+void launch_peer_barrier(const PeerBarrier& b, cudaStream_t s);
 
 void launch_memset_zero(void* p, size_t bytes, cudaStream_t s);
 // one thread spinning ~cycles clocks (delay injection on the comm stream, tests only)

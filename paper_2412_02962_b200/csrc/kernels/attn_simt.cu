@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) attn_simt_kernel(const AttnArgs a) {
 
   for (int s = 0; s < a.nsrc; ++s) {
     const T* KV = reinterpret_cast<const T*>(a.src[s].kv);
-    const int nk = a.src[s].rows * a.W;
+    const int nk = a.src[s].nkeys > 0 ? min(a.src[s].nkeys, a.src[s].rows * a.W) : a.src[s].rows * a.W;
     for (int k0 = 0; k0 < nk; k0 += KC) {
       __syncthreads();
       for (int e = tid; e < KC * HD; e += 256) {

@@ -24,6 +24,7 @@ namespace pcpp {
 struct TcAttnParams {
   CUtensorMap mq, mkv[3];
   int nsrc, rows[3];
+  int nkeys[3];               // keys attended per source (token order r * W + w); rows * W unless masked
   int h, W, B, C;
   int Wbox, Rbox, nWt, ntiles;
   unsigned box_bytes;
@@ -223,7 +224,8 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
         if (j > 0 && (w0 += p.Wbox) >= p.W) { w0 = 0; if ((r0 += p.Rbox) >= p.rows[s]) { r0 = 0; ++s; } }
         const int nvr = min(p.Rbox, p.rows[s] - r0);
         const int nvw = min(p.Wbox, p.W - w0);
-        const int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;   // valid keys form a prefix
+        int nvalid = p.Rbox == 1 ? (nvr > 0 ? nvw : 0) : nvr * p.Wbox;   // valid keys form a prefix
+        nvalid = min(nvalid, max(0, p.nkeys[s] - (r0 * p.W + w0)));          // masked tail (context keys)
         sm100::mbar_wait(&s_full[g], j & 1);
         sm100::fence_after();
         // pass 1: row max.  Columns 64-127 stay in registers; 0-63 are re-read in pass 2, after
@@ -367,36 +369,6 @@ static bool encode_tok(CUtensorMap* m, const void* base, int rows, int B, int W,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// split-KV combine: O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s, M = max_s m_s (fixed order)
-__global__ void attn_combine_kernel(const float* __restrict__ ws, int nsplit, int B, int heads, int h, int W,
-                                    int C, bf16* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  const long long ntok = (long long)h * W;
-  const long long total = (long long)B * heads * ntok;
-  for (long long i = (long long)blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8; i < total;
-       i += (long long)gridDim.x * (blockDim.x / 8)) {
-    const int part = threadIdx.x & 7;                 // 8 threads per row, 8 dims each
-    const long long tok = i % ntok;
-    const int head = (int)((i / ntok) % heads), b = (int)(i / (ntok * heads));
-    float M = -INFINITY;
-    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, ws[(((long long)s * B + b) * heads + head) * ntok * 66 + tok * 66 + 64]);
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, L = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float* wp = ws + ((((long long)s * B + b) * heads + head) * ntok + tok) * 66;
-      const float f = exp2f(wp[64] - M);
-      L += f * wp[65];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += f * wp[part * 8 + e];
-    }
-    const float inv = 1.f / L;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] *= inv;
-    const int r = (int)(tok / W), w = (int)(tok % W);
-    store8(out + (((long long)r * B + b) * W + w) * C + head * 64 + part * 8, acc);
-  }
-}
-
 bool attn_tc_supported(const AttnArgs& a) {
   if (a.dtype != DT_BF16 || a.C % 64 || a.nsrc < 1) return false;
   if (!tma_encode_fn()) return false;
@@ -404,7 +376,6 @@ bool attn_tc_supported(const AttnArgs& a) {
 }
 
 void attn_tc_init() {
-  cudaFuncSetAttribute(attn_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg<2>::SMEM);
   cudaFuncSetAttribute(attn_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnCfg<1>::SMEM);
 }
 
@@ -424,46 +395,18 @@ bool launch_attn_tc(const AttnArgs& a, cudaStream_t s) {
     if (a.src[i].rows <= 0) continue;
     if (!encode_tok(&p.mkv[p.nsrc], a.src[i].kv, a.src[i].rows, a.B, a.W, 2 * a.C, p.Wbox, p.Rbox)) return false;
     p.rows[p.nsrc] = a.src[i].rows;
+    p.nkeys[p.nsrc] = a.src[i].nkeys > 0 ? a.src[i].nkeys : a.src[i].rows * a.W;
     p.ntiles += ((a.src[i].rows + p.Rbox - 1) / p.Rbox) * p.nWt;
     p.nsrc++;
   }
   for (int i = p.nsrc; i < 3; ++i) p.mkv[i] = p.mkv[0];
   const int qtiles = ((a.h + p.Rbox - 1) / p.Rbox) * p.nWt;
-  const long long ctas = (long long)((qtiles + 1) / 2) * (a.C / 64) * a.B;
-  // split the key range when the (q tile pair, head, b) grid under-fills the 148 SMs
+  // one 128-query tile per CTA, two single-warpgroup CTAs per SM (NWG = 1): measured 10 % faster over
+  // the 1024^2 step than one CTA with two ping-pong warpgroups, and faster than split-KV + combine
+  // at every 1024^2 shape (round-1 A/B)
   p.nsplit = 1; p.ws = a.ws;
-  // split-KV (+ combine) is off by default: measured slower than the unsplit kernel at every
-  // 1024^2 shape (per-CTA prologue + combine); PCPP_ATTN_SPLIT=1 enables it for experiments
-  static const int split_env = getenv("PCPP_ATTN_SPLIT") ? atoi(getenv("PCPP_ATTN_SPLIT")) : 0;
-  if (a.ws && split_env) {
-    double best = (double)ctas / (double)(((ctas + 147) / 148) * 148);
-    for (int sp = 2; sp <= 8; ++sp) {
-      if (p.ntiles / sp < 3) break;
-      const long long need = (long long)sp * a.B * (a.C / 64) * a.h * a.W * 66;
-      if ((size_t)need > a.ws_elems) break;
-      const long long c = ctas * sp;
-      const double e = (double)c / (double)(((c + 147) / 148) * 148) - 0.03 * (sp - 1);
-      if (e > best + 0.05) { best = e; p.nsplit = sp; }
-    }
-  }
-  // query tiles per CTA (PCPP_ATTN_NWG): 1 (default) = two single-warpgroup CTAs per SM -- measured
-  // 10 % faster over the 1024^2 step than 2 = one CTA per SM with two ping-pong warpgroups (finer
-  // grid: the 2.16-wave level-1 and 1.08-wave level-2 grids lose less to the tail wave)
-  static const int nwg_env = getenv("PCPP_ATTN_NWG") ? atoi(getenv("PCPP_ATTN_NWG")) : 1;
-  if (nwg_env == 1 && p.nsplit == 1) {
-    dim3 grid(qtiles, a.C / 64, a.B);
-    launch_pdl(attn_tc_kernel<1>, grid, dim3(AttnCfg<1>::THREADS), AttnCfg<1>::SMEM, s, p);
-  } else {
-    dim3 grid((qtiles + 1) / 2, a.C / 64, a.B * p.nsplit);
-    launch_pdl(attn_tc_kernel<2>, grid, dim3(AttnCfg<2>::THREADS), AttnCfg<2>::SMEM, s, p);
-  }
-  if (p.nsplit > 1) {
-    const long long rows = (long long)a.B * (a.C / 64) * a.h * a.W;
-    long long blocks = (rows + 31) / 32;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    launch_pdl(attn_combine_kernel, dim3((unsigned)blocks), dim3(256), 0, s, p.ws, p.nsplit, a.B, a.C / 64, a.h, a.W, a.C,
-                                                         reinterpret_cast<bf16*>(a.out));
-  }
+  dim3 grid(qtiles, a.C / 64, a.B);
+  launch_pdl(attn_tc_kernel<1>, grid, dim3(AttnCfg<1>::THREADS), AttnCfg<1>::SMEM, s, p);
   return true;
 }
 

@@ -213,49 +213,6 @@ bool launch_conv_in(const GemmArgs& g, cudaStream_t s) {
   return true;
 }
 
-// conv_out for bf16 activations: lane = output token (128 consecutive tokens of one row per CTA),
-// the 9 x C x 4 fp32 weights staged once per CTA in shared memory as [tap * C + c][4] so one
-// broadcast 16-byte read feeds the 4 output channels; activations read as 16-byte channel vectors.
-__global__ void __launch_bounds__(128) conv_out_bf16_kernel(const ActView in, const float* __restrict__ w,
-                                                            const float* __restrict__ bias, const ActView out) {
-  pdl_trigger();
-  extern __shared__ float4 wsm[];                 // [9 * C] x {o0, o1, o2, o3}
-  const int C = in.C, K = 9 * C;
-  for (int i = threadIdx.x; i < K; i += blockDim.x)
-    wsm[i] = make_float4(w[i], w[K + i], w[2 * K + i], w[3 * K + i]);
-  __syncthreads();
-  pdl_wait();
-  const int nwt = (out.W + 127) / 128;
-  const int wt = blockIdx.x % nwt;
-  const int rb = blockIdx.x / nwt;                 // r * B + b
-  const int b = rb % out.B, r = rb / out.B;
-  const int wo = wt * 128 + threadIdx.x;
-  if (wo >= out.W) return;
-  const bf16* x = reinterpret_cast<const bf16*>(in.base);
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 1
-  for (int tap = 0; tap < 9; ++tap) {
-    const int ri = r + tap / 3 - 1, wi = wo + tap % 3 - 1;
-    if (wi < 0 || wi >= in.W) continue;                // zero padding left / right (halo rows exist)
-    const uint4* px = reinterpret_cast<const uint4*>(x + (((long long)ri * in.B + b) * in.W + wi) * C);
-    const float4* pw = wsm + tap * C;
-#pragma unroll 2
-    for (int c8 = 0; c8 < C / 8; ++c8) {
-      const uint4 u = __ldg(px + c8);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h[e]);
-        const float4 w0 = pw[c8 * 8 + 2 * e], w1 = pw[c8 * 8 + 2 * e + 1];
-        a0 = fmaf(f.x, w0.x, a0); a1 = fmaf(f.x, w0.y, a1); a2 = fmaf(f.x, w0.z, a2); a3 = fmaf(f.x, w0.w, a3);
-        a0 = fmaf(f.y, w1.x, a0); a1 = fmaf(f.y, w1.y, a1); a2 = fmaf(f.y, w1.z, a2); a3 = fmaf(f.y, w1.w, a3);
-      }
-    }
-  }
-  float4* po = reinterpret_cast<float4*>(reinterpret_cast<float*>(out.base) + (((long long)r * out.B + b) * out.W + wo) * 4);
-  *po = make_float4(a0 + bias[0], a1 + bias[1], a2 + bias[2], a3 + bias[3]);
-}
-
 // conv_out v3 (bf16 in, Cin -> 4, fp32 out): the 9*Cin x 4 weights are staged in smem as float4 over
 // the 4 outputs, laid out [e][chunk] (chunk = tap * Cin/8 + c/8, e = channel within the 8-channel
 // chunk) so a warp's 32 lanes read 32 consecutive float4 (no bank conflicts).  A warp computes 4
@@ -330,17 +287,7 @@ __global__ void __launch_bounds__(256) conv_out_v3_kernel(const ActView in, cons
 }
 
 void launch_conv_out(const ActView& in, const float* w, const float* bias, const ActView& out, cudaStream_t s) {
-  static const int v2 = getenv("PCPP_CONV_OUT_V2") ? atoi(getenv("PCPP_CONV_OUT_V2")) : 0;   // measured slower
-  if (v2 && in.dtype == DT_BF16 && in.C % 8 == 0 && out.C == 4 && (size_t)in.C * 9 * 16 <= 160 * 1024) {
-    static bool attr = false;
-    if (!attr) { cudaFuncSetAttribute(conv_out_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); attr = true; }
-    const int nwt = (out.W + 127) / 128;
-    launch_pdl(conv_out_bf16_kernel, dim3((unsigned)(out.rows * out.B * nwt)), dim3(128), (size_t)in.C * 9 * 16, s, in, w,
-               bias, out);
-    return;
-  }
-  static const int v3 = getenv("PCPP_CONV_OUT_V3") ? atoi(getenv("PCPP_CONV_OUT_V3")) : 1;
-  if (v3 && in.dtype == DT_BF16 && in.C % 8 == 0 && out.C == 4 && out.W % 4 == 0 && (size_t)in.C * 9 * 16 <= 48 * 1024) {
+  if (in.dtype == DT_BF16 && in.C % 8 == 0 && out.C == 4 && out.W % 4 == 0 && (size_t)in.C * 9 * 16 <= 48 * 1024) {
     const long long ngroups = (long long)out.rows * out.B * (out.W / 4);
     const long long blocks = std::min<long long>((ngroups + 7) / 8, 148 * 2);
     launch_pdl(conv_out_v3_kernel, dim3((unsigned)blocks), dim3(256), (size_t)in.C * 9 * 16, s, in, w, bias, out);

@@ -32,15 +32,15 @@ struct TcGemmParams {
   ActView res, out, out2;
   int splits, s_len;          // split-K: blockIdx.z covers k-steps [z*s_len, (z+1)*s_len)
   float* ws;                  // [splits][M][N] fp32 partials (M = tokens in layout order)
-  int epi_skip;               // experiment only (PCPP_EPI_SKIP): drop the epilogue math/stores
-  float* gn_part;             // fused GroupNorm statistics: [gridDim.x * 4 warps][B=2][G=32][2] fp32
+  double* gn_part;            // fused GroupNorm statistics: [gridDim.x * 4 warps][B=2][G=32][2] fp64
   int gn_cg;                  //   channels per group (N / 32)
 };
 
 // Extra shared memory of the stats-fused variant: per epilogue warp a 32 x 17-word bf16 transpose
-// tile (conflict-free row writes / column reads) and the warp's [2][32][2] fp32 group accumulators.
+// tile (conflict-free row writes / column reads) and the warp's [2][32][2] fp64 group accumulators
+// (fp64 across tiles: the E[x^2] - mu^2 form loses digits when a group's mean is large against its std).
 constexpr int ST_TILE_WORDS = 32 * 17;
-constexpr int ST_SMEM = 4 * ST_TILE_WORDS * 4 + 4 * 128 * 4;
+constexpr int ST_SMEM = 4 * ST_TILE_WORDS * 4 + 4 * 128 * 8;
 
 template <int BN, bool ST = false>
 struct TcCfg {
@@ -98,7 +98,7 @@ __device__ __forceinline__ void res_prefetch(const TcGemmParams& p, long long rr
 // bf16 outputs as stored): transpose through smem so lane j sums column j over the 32 rows, then a
 // segmented suffix scan over lanes of the same group; the group's first lane adds into the warp's
 // accumulator sacc[b][g][{sum, sumsq}].  Fixed order everywhere (deterministic).
-__device__ __forceinline__ void gn_chunk_stats(uint32_t* stile, float* sacc, const uint32_t* u, int b, unsigned bmask,
+__device__ __forceinline__ void gn_chunk_stats(uint32_t* stile, double* sacc, const uint32_t* u, int b, unsigned bmask,
                                                int col0, int cg) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -132,10 +132,10 @@ __device__ __forceinline__ void gn_chunk_stats(uint32_t* stile, float* sacc, con
   }
   if (lane == 0 || rem == cg - 1) {
     if (!mixed) {
-      float* a = sacc + (b * 32 + g) * 2;
+      double* a = sacc + (b * 32 + g) * 2;
       a[0] += s0; a[1] += q0;
     } else {
-      float* a = sacc + g * 2;
+      double* a = sacc + g * 2;
       a[0] += s0; a[1] += q0; a[64] += s1; a[65] += q1;
     }
   }
@@ -149,7 +149,7 @@ __device__ __forceinline__ long long res_row(const TcGemmParams& p, int r, int b
 // rres0: the residual of chunk 0, prefetched by the caller before it waited for the accumulator
 template <int BN, bool ST>
 __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t tacc, int r, int b, int w, bool valid,
-                                              int n0, int z, uint32_t* stile, float* sacc, unsigned bmask,
+                                              int n0, int z, uint32_t* stile, double* sacc, unsigned bmask,
                                               const uint4* rres0) {
   const bool second = n0 >= p.n_split;
   const ActView& ov = second ? p.out2 : p.out;
@@ -204,7 +204,7 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
         for (int j = 0; j < 4; ++j) rcur[j] = rnext[j];
         continue;
       }
-      if (!valid || p.epi_skip) continue;
+      if (!valid) continue;
       float f[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   uint64_t* tempty = tfull + 2;              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* st_tile = reinterpret_cast<uint32_t*>(smem + Cfg::STAGES * Cfg::STAGE + 256);   // ST only
-  float* st_acc = reinterpret_cast<float*>(st_tile + 4 * ST_TILE_WORDS);
+  double* st_acc = reinterpret_cast<double*>(st_tile + 4 * ST_TILE_WORDS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -339,10 +339,10 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
     uint32_t* stile = st_tile + q * ST_TILE_WORDS;
-    float* sacc = st_acc + q * 128;
+    double* sacc = st_acc + q * 128;
     if (ST) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) sacc[lane * 4 + i] = 0.f;
+      for (int i = 0; i < 4; ++i) sacc[lane * 4 + i] = 0.0;
       __syncwarp();
     }
     int tc = 0;
@@ -364,8 +364,8 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
     }
     if (ST) {
-      const float4 v = *reinterpret_cast<const float4*>(sacc + lane * 4);
-      *reinterpret_cast<float4*>(p.gn_part + ((size_t)blockIdx.x * 4 + q) * 128 + lane * 4) = v;
+      const double4 v = *reinterpret_cast<const double4*>(sacc + lane * 4);
+      *reinterpret_cast<double4*>(p.gn_part + ((size_t)blockIdx.x * 4 + q) * 128 + lane * 4) = v;
     }
   }
   sm100::fence_before();
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
   uint64_t* tempty = tfull + 2;              // [2] (leader's counts both CTAs' epilogue warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* st_tile = reinterpret_cast<uint32_t*>(smem + Cfg::STAGES * Cfg::STAGE + 256);   // ST only
-  float* st_acc = reinterpret_cast<float*>(st_tile + 4 * ST_TILE_WORDS);
+  double* st_acc = reinterpret_cast<double*>(st_tile + 4 * ST_TILE_WORDS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_rank();
@@ -584,10 +584,10 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
     uint32_t* stile = st_tile + q * ST_TILE_WORDS;
-    float* sacc = st_acc + q * 128;
+    double* sacc = st_acc + q * 128;
     if (ST) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) sacc[lane * 4 + i] = 0.f;
+      for (int i = 0; i < 4; ++i) sacc[lane * 4 + i] = 0.0;
       __syncwarp();
     }
     int tc = 0;
@@ -608,8 +608,8 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
     }
     if (ST) {
-      const float4 v = *reinterpret_cast<const float4*>(sacc + lane * 4);
-      *reinterpret_cast<float4*>(p.gn_part + ((size_t)blockIdx.x * 4 + q) * 128 + lane * 4) = v;
+      const double4 v = *reinterpret_cast<const double4*>(sacc + lane * 4);
+      *reinterpret_cast<double4*>(p.gn_part + ((size_t)blockIdx.x * 4 + q) * 128 + lane * 4) = v;
     }
   }
   sm100::fence_before();
@@ -737,8 +737,6 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   p.a_bytes = 128u * p.Wbox * p.Bbox * p.Rbox;
   p.bias = g.bias; p.temb = g.temb; p.temb_ld = g.temb_ld;
   p.res = g.res; p.out = g.out; p.out2 = g.out2;
-  static const int epi_skip = getenv("PCPP_EPI_SKIP") ? atoi(getenv("PCPP_EPI_SKIP")) : 0;
-  p.epi_skip = epi_skip;
   if (!encode_act(&p.ma0, g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_act(&p.ma1, g.a1.base ? g.a1 : g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN)) return false;
@@ -789,8 +787,7 @@ static GemmChoice heuristic(const GemmArgs& g) {
   const long long tiles = (long long)m_tiles * (g.N / c.bn);
   const int nsteps = g.taps * (g.cin / 64);
   const long long M = (long long)g.rows_out * g.B * g.w_out;
-  static const int splitk_env = getenv("PCPP_SPLITK") ? atoi(getenv("PCPP_SPLITK")) : 1;
-  if (splitk_env && g.ws && tiles < 148) {
+  if (g.ws && tiles < 148) {
     double best = wave_eff(tiles);
     for (int S = 2; S <= 8; ++S) {
       if (nsteps / S < 8) break;
@@ -860,8 +857,7 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
   GemmChoice best = heuristic(g);
   float best_ms = 1e30f;
   const int bns[4] = {256, 160, 128, 64};
-  static const int pair_env = getenv("PCPP_PAIR") ? atoi(getenv("PCPP_PAIR")) : 1;
-  for (int pair = 0; pair <= (pair_env ? 1 : 0); ++pair)
+  for (int pair = 0; pair <= 1; ++pair)
   for (int bn : bns) {
     if (!bn_ok(g, bn)) continue;
     if (pair && bn == 64) continue;

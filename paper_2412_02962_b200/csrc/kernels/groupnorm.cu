@@ -16,24 +16,24 @@ namespace pcpp {
 
 namespace {
 constexpr int G = 32;
-constexpr int NT = 256;
+constexpr int NT = 512;
 
 struct Lanes { int nv, vpt, nvl, ntl; };
 __host__ __device__ __forceinline__ Lanes lanes_for(int C) {
   Lanes L;
   L.nv = C / 8;
-  L.vpt = (L.nv + NT - 1) / NT;          // vectors per thread (1 or 2)
+  L.vpt = (L.nv + NT - 1) / NT;          // vectors per thread (1 for C <= 4096)
   L.nvl = (L.nv + L.vpt - 1) / L.vpt;    // distinct vector lanes
   L.ntl = NT / L.nvl;                    // token lanes
   return L;
 }
 }  // namespace
 
-int gn_stats_chunks(int rows, int W) {   // CTAs of gn_stats (each covers both CFG branches)
+int gn_stats_chunks(int rows, int W) {   // CTAs of gn_stats: >= 64 tokens each, at most one wave
   long long tok = (long long)rows * 2 * W;
-  long long c = tok / 32;                 // >= 32 tokens per chunk
+  long long c = tok / 64;
   if (c < 1) c = 1;
-  if (c > 296) c = 296;                   // 2 CTAs per SM
+  if (c > 148) c = 148;
   return (int)c;
 }
 
@@ -43,11 +43,16 @@ __device__ __forceinline__ const T* vptr(const ActView& v, long long rowtok, int
 }
 
 // ---- stats -------------------------------------------------------------------------------------
-// CTA `chunk` covers layout tokens [T0, T1) (all (r, b, w) in memory order: address T*C + c, no
-// index division); token lanes stride by ntl, 4 independent 16 B loads in flight per thread.
-// returns true in the CTA that arrived last (it has reduced the partials into a.m_out)
+// One wave of <= 148 CTAs; CTA `chunk` covers layout tokens [T0, T1) (all (r, b, w) in memory order:
+// address T*C + c).  Thread = (fixed 8-channel vector lane, token lane); token lanes stride by ntl
+// with 4 independent 16 B loads in flight; per-thread fp32 sums over its few tokens, then a
+// fixed-order per-(b, g) reduction in fp64 into the CTA's partial slot partial[chunk][B=2][G][2].
+// The slots are summed by gn_finalize (the same finalize as the GEMM-epilogue-fused statistics).
 template <typename T>
-__device__ __forceinline__ bool gn_stats_phase(const GnStatsArgs& a, float* red, bool& amlast) {
+__global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ float red[];                   // [ntl][nv][2 b][8][2]
   const int chunk = blockIdx.x;
   const int W = a.x0.W, B = a.x0.B, C = a.C;
   const Lanes L = lanes_for(C);
@@ -55,120 +60,75 @@ __device__ __forceinline__ bool gn_stats_phase(const GnStatsArgs& a, float* red,
   const int vl = tid % L.nvl, tl = tid / L.nvl;
   const long long ntok = (long long)a.x0.rows * B * W;
   const long long T0 = ntok * chunk / a.nchunk, T1 = ntok * (chunk + 1) / a.nchunk;
-  float s[2][2][8], q[2][2][8];                    // [u][b][e]
-#pragma unroll
-  for (int u = 0; u < 2; ++u)
+  const int v = vl * L.vpt;                        // vpt == 1 for every supported C
+  if (tl < L.ntl && v < L.nv) {
+    float s[2][8], q[2][8];
 #pragma unroll
     for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) { s[u][bb][e] = 0.f; q[u][bb][e] = 0.f; }
-  if (tl < L.ntl) {
+      for (int e = 0; e < 8; ++e) { s[bb][e] = 0.f; q[bb][e] = 0.f; }
+    const int c = v * 8;
+    const bool second = c >= a.c0;
+    const ActView& src = second ? a.x1 : a.x0;
+    const int cc = second ? c - a.c0 : c;
+    long long Tt = T0 + tl;
+    int w = (int)(Tt % W), bq = (int)((Tt / W) % B);
+    for (; Tt < T1; Tt += 4LL * L.ntl) {
+      float x[4][8];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int v = vl * L.vpt + u;
-      if (u >= L.vpt || v >= L.nv) continue;
-      const int c = v * 8;
-      const bool second = c >= a.c0;
-      const ActView& src = second ? a.x1 : a.x0;
-      const int cc = second ? c - a.c0 : c;
-      long long Tt = T0 + tl;
-      int w = (int)(Tt % W), bq = (int)((Tt / W) % B);
-      for (; Tt < T1; Tt += 4LL * L.ntl) {
-        float x[4][8];
+      for (int k = 0; k < 4; ++k) {
+        const long long Tk = Tt + (long long)k * L.ntl;
+        if (Tk < T1) load8(vptr<T>(src, Tk, cc), x[k]);
+        else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const long long Tk = Tt + (long long)k * L.ntl;
-          if (Tk < T1) load8(vptr<T>(src, Tk, cc), x[k]);
-          else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) x[k][e] = 0.f;
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (bq == 0) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) { s[u][0][e] += x[k][e]; q[u][0][e] = fmaf(x[k][e], x[k][e], q[u][0][e]); }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) { s[u][1][e] += x[k][e]; q[u][1][e] = fmaf(x[k][e], x[k][e], q[u][1][e]); }
-          }
-          w += L.ntl;
-          while (w >= W) { w -= W; bq = (bq + 1 == B) ? 0 : bq + 1; }
+          for (int e = 0; e < 8; ++e) x[k][e] = 0.f;
         }
       }
-    }
-  }
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int v = vl * L.vpt + u;
-    if (u < L.vpt && tl < L.ntl && v < L.nv)
+      for (int k = 0; k < 4; ++k) {
+        if (bq == 0) {
 #pragma unroll
-      for (int bb = 0; bb < 2; ++bb)
+          for (int e = 0; e < 8; ++e) { s[0][e] += x[k][e]; q[0][e] = fmaf(x[k][e], x[k][e], q[0][e]); }
+        } else {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          red[(((long long)tl * L.nv + v) * 2 + bb) * 16 + e * 2 + 0] = s[u][bb][e];
-          red[(((long long)tl * L.nv + v) * 2 + bb) * 16 + e * 2 + 1] = q[u][bb][e];
+          for (int e = 0; e < 8; ++e) { s[1][e] += x[k][e]; q[1][e] = fmaf(x[k][e], x[k][e], q[1][e]); }
         }
+        w += L.ntl;
+        while (w >= W) { w -= W; bq = (bq + 1 == B) ? 0 : bq + 1; }
+      }
+    }
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        red[(((long long)tl * L.nv + v) * 2 + bb) * 16 + e * 2 + 0] = s[bb][e];
+        red[(((long long)tl * L.nv + v) * 2 + bb) * 16 + e * 2 + 1] = q[bb][e];
+      }
   }
   __syncthreads();
   const int cg = C / G;
-  if (tid < B * G * 2) {                             // fixed-order per-(b, g, stat) sums -> partial [B][G][2][nchunk]
+  if (tid < 2 * G * 2) {                             // fixed-order per-(b, g, stat) sums -> this CTA's slot
     const int bb = tid / (2 * G), g = (tid >> 1) % G, k = tid & 1;
     double acc = 0.0;
-    for (int c = g * cg; c < (g + 1) * cg; ++c) {
-      const int v = c / 8, e = c % 8;
-      for (int l = 0; l < L.ntl; ++l) acc += red[(((long long)l * L.nv + v) * 2 + bb) * 16 + e * 2 + k];
-    }
-    a.partial[(((long long)bb * G + g) * 2 + k) * a.nchunk + chunk] = acc;
+    if (bb < B)
+      for (int c = g * cg; c < (g + 1) * cg; ++c) {
+        const int vv = c / 8, e = c % 8;
+        for (int l = 0; l < L.ntl; ++l) acc += red[(((long long)l * L.nv + vv) * 2 + bb) * 16 + e * 2 + k];
+      }
+    a.partial[(size_t)chunk * 128 + tid] = acc;      // [slot][b][g][2]
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) amlast = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!amlast) return false;
-  __threadfence();
-  // last CTA: 2*B*G sums over nchunk partials; warp-per-sum, lane-strided loads, fixed-order tree
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int i = warp; i < B * G * 2; i += NT / 32) {
-    const double* pp = a.partial + (long long)i * a.nchunk;
-    double acc = 0.0;
-    for (int c = lane; c < a.nchunk; c += 32) acc += __ldcg(pp + c);
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-    if (lane == 0) a.m_out[i] = acc;                  // [B][G][2]
-  }
-  if (tid == 0) *a.counter = 0u;                      // ready for the next launch / graph replay
-  return true;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ float red[];                   // [ntl][nv][2 b][8][2]
-  __shared__ bool amlast;
-  gn_stats_phase<T>(a, red, amlast);
-}
-
-
-void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
-  const Lanes L = lanes_for(a.C);
-  const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
-  if (a.x0.dtype == DT_F32) launch_pdl(gn_stats_kernel<float>, dim3(a.nchunk), dim3(NT), smem, s, a);
-  else launch_pdl(gn_stats_kernel<bf16>, dim3(a.nchunk), dim3(NT), smem, s, a);
 }
 
 // ---- finalize of the GEMM-fused statistics ------------------------------------------------------
 // CTA (b, g): 128 threads stride over the slots in fp64, then a fixed-order tree.
-__global__ void __launch_bounds__(128) gn_finalize_kernel(const float* __restrict__ part, int nslots,
+__global__ void __launch_bounds__(128) gn_finalize_kernel(const double* __restrict__ part, int nslots,
                                                           double* __restrict__ m_out) {
   pdl_trigger();
   pdl_wait();
   const int i = blockIdx.x;                  // b * G + g
   double s = 0.0, q = 0.0;
   for (int k = threadIdx.x; k < nslots; k += 128) {
-    const float2 v = __ldcg(reinterpret_cast<const float2*>(part + (size_t)k * 128) + i);
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(part + (size_t)k * 128) + i);
     s += v.x; q += v.y;
   }
 #pragma unroll
@@ -183,8 +143,17 @@ __global__ void __launch_bounds__(128) gn_finalize_kernel(const float* __restric
   }
 }
 
-void launch_gn_finalize(const float* part, int nslots, double* m_out, cudaStream_t s) {
+void launch_gn_finalize(const double* part, int nslots, double* m_out, cudaStream_t s) {
   launch_pdl(gn_finalize_kernel, dim3(2 * G), dim3(128), 0, s, part, nslots, m_out);
+}
+
+// stats pass over x (+ x1 for a channel concat) and the finalize of its per-CTA slots
+void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
+  const Lanes L = lanes_for(a.C);
+  const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
+  if (a.x0.dtype == DT_F32) launch_pdl(gn_stats_kernel<float>, dim3(a.nchunk), dim3(NT), smem, s, a);
+  else launch_pdl(gn_stats_kernel<bf16>, dim3(a.nchunk), dim3(NT), smem, s, a);
+  launch_gn_finalize(a.partial, a.nchunk, a.m_out, s);
 }
 
 // ---- apply -------------------------------------------------------------------------------------
@@ -208,132 +177,6 @@ __device__ __forceinline__ void gn_prep(const GnApplyArgs& a, float* mu_s, float
     mu_s[i] = (float)mu;
     rs_s[i] = (float)(1.0 / sqrt(var + 1e-5));
   }
-}
-
-template <typename TI, typename TO>
-__device__ __forceinline__ void gn_apply_phase(const GnApplyArgs& a, const float* mu_s, const float* rs_s,
-                                               long long T0, long long T1) {
-  const int B = a.x0.B;
-  const int C = a.C, cg = C / G, W = a.x0.W;
-  const Lanes L = lanes_for(C);
-  const int vl = threadIdx.x % L.nvl, tl = threadIdx.x / L.nvl;
-  if (tl >= L.ntl) return;
-  // per-thread affine y = x * A[b][e] + Bc[b][e] for its (<= 2) vectors
-  float A[2][2][8], Bc[2][2][8];
-  int cvec[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int v = vl * L.vpt + u;
-    cvec[u] = (u < L.vpt && v < L.nv) ? v * 8 : -1;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int ch = cvec[u] < 0 ? 0 : cvec[u] + e, g = ch / cg;
-      const float ga = a.gamma[ch], be = a.beta[ch];
-#pragma unroll
-      for (int bb = 0; bb < 2; ++bb) {
-        const int bi = bb < B ? bb : 0;
-        const float rs = rs_s[bi * G + g] * ga;
-        A[u][bb][e] = rs;
-        Bc[u][bb][e] = be - mu_s[bi * G + g] * rs;
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    if (cvec[u] < 0) continue;
-    const int c = cvec[u];
-    const bool second = c >= a.c0;
-    const ActView& src = second ? a.x1 : a.x0;
-    const int cc = second ? c - a.c0 : c;
-    long long T = T0 + tl;
-    int w = (int)(T % W), bq = (int)((T / W) % B);
-    for (; T < T1; T += 4LL * L.ntl) {
-      float x[4][8];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const long long Tk = T + (long long)k * L.ntl;
-        if (Tk < T1) load8(vptr<TI>(src, Tk, cc), x[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const long long Tk = T + (long long)k * L.ntl;
-        if (bq) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[k][e] = fmaf(x[k][e], A[u][1][e], Bc[u][1][e]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[k][e] = fmaf(x[k][e], A[u][0][e], Bc[u][0][e]);
-        }
-        if (a.silu) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[k][e] = silu_f(x[k][e]);
-        }
-        // out has the same (r, b, w) geometry; it may be a padded tensor (base = row 0)
-        if (Tk < T1) store8(reinterpret_cast<TO*>(a.out.base) + Tk * a.out.C + c, x[k]);
-        w += L.ntl;
-        while (w >= W) { w -= W; bq = (bq + 1 == B) ? 0 : bq + 1; }
-      }
-    }
-  }
-}
-
-template <typename TI, typename TO>
-__global__ void __launch_bounds__(NT) gn_apply_kernel(const GnApplyArgs a, int tok_per_cta) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float mu_s[2 * G], rs_s[2 * G];
-  gn_prep(a, mu_s, rs_s);
-  __syncthreads();
-  const long long ntok = (long long)a.x0.rows * a.x0.B * a.x0.W;   // (r, b, w) tokens in layout order
-  const long long T0 = (long long)blockIdx.x * tok_per_cta;
-  const long long T1 = T0 + tok_per_cta < ntok ? T0 + tok_per_cta : ntok;
-  gn_apply_phase<TI, TO>(a, mu_s, rs_s, T0, T1);
-}
-
-// Stats + apply in one launch (n = 1 and async steps: the apply needs only this rank's fresh sums
-// and the previous step's exchanged sums).  The last CTA to finish the stats phase reduces the
-// partials and bumps a generation word; the others wait for it (all CTAs are co-resident: grid
-// <= 148).  Phase 2 re-reads this CTA's own token range (L2-resident).
-template <typename TI, typename TO>
-__global__ void __launch_bounds__(NT) gn_fused_kernel(const GnStatsArgs sa, const GnApplyArgs aa) {
-  pdl_trigger();
-  pdl_wait();
-  extern __shared__ float red[];
-  __shared__ bool amlast;
-  __shared__ float mu_s[2 * G], rs_s[2 * G];
-  volatile unsigned* gen = sa.counter + 1;
-  unsigned g0 = 0;
-  if (threadIdx.x == 0) g0 = *gen;
-  __syncthreads();
-  const bool last = gn_stats_phase<TI>(sa, red, amlast);
-  if (last) __threadfence();               // every writer of m_out fences before the signal
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (last) { __threadfence(); atomicAdd(sa.counter + 1, 1u); }
-    else {
-      const long long t0 = clock64();
-      while (*gen == g0) {
-        __nanosleep(64);
-        if (clock64() - t0 > 20000000000LL) __trap();
-      }
-      __threadfence();
-    }
-  }
-  __syncthreads();
-  gn_prep(aa, mu_s, rs_s);
-  __syncthreads();
-  const long long ntok = (long long)sa.x0.rows * sa.x0.B * sa.x0.W;
-  const long long T0 = ntok * blockIdx.x / sa.nchunk, T1 = ntok * (blockIdx.x + 1) / sa.nchunk;
-  gn_apply_phase<TI, TO>(aa, mu_s, rs_s, T0, T1);
-}
-
-void launch_gn_fused(const GnStatsArgs& sa, const GnApplyArgs& aa, cudaStream_t s) {
-  GnStatsArgs a2 = sa;
-  if (a2.nchunk > 148) a2.nchunk = 148;
-  const Lanes L = lanes_for(a2.C);
-  const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
-  if (a2.x0.dtype == DT_F32) launch_pdl(gn_fused_kernel<float, float>, dim3(a2.nchunk), dim3(NT), smem, s, a2, aa);
-  else launch_pdl(gn_fused_kernel<bf16, bf16>, dim3(a2.nchunk), dim3(NT), smem, s, a2, aa);
 }
 
 // Wide apply: every thread of the grid owns one fixed 8-channel vector lane v = gid % nv (so its
@@ -401,33 +244,20 @@ __global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a,
 }
 
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
-  static const int wide = getenv("PCPP_GN_WIDE") ? atoi(getenv("PCPP_GN_WIDE")) : 1;
-  if (wide && a.C % 8 == 0 && a.x0.B <= 2 && (a.x1.base == nullptr || a.c0 % 8 == 0)) {
-    const int nv = a.C / 8;
-    const long long ntok = (long long)a.x0.rows * a.x0.B * a.x0.W;
-    long long blocks = (ntok * nv + 512 * 4 - 1) / (512 * 4);
-    if (blocks > 148 * 2) blocks = 148 * 2;
-    if (blocks < 1) blocks = 1;
-    int lanes = (int)(blocks * 512 / nv);
-    if (lanes < 1) { lanes = 1; blocks = (nv + 511) / 512; }
-    if (a.x0.dtype == DT_F32) launch_pdl(gn_apply_wide_kernel<float, float>, dim3((unsigned)blocks), dim3(512), 0, s, a, lanes);
-    else launch_pdl(gn_apply_wide_kernel<bf16, bf16>, dim3((unsigned)blocks), dim3(512), 0, s, a, lanes);
-    return;
-  }
-  const Lanes L = lanes_for(a.C);
+  const int nv = a.C / 8;
   const long long ntok = (long long)a.x0.rows * a.x0.B * a.x0.W;
-  long long per = (long long)L.ntl * 8;                           // ~8 tokens per token lane
-  long long blocks = (ntok + per - 1) / per;
-  if (blocks > 148 * 8) { blocks = 148 * 8; per = (ntok + blocks - 1) / blocks; }
-  if (a.x0.dtype == DT_F32) launch_pdl(gn_apply_kernel<float, float>, dim3((unsigned)blocks), dim3(NT), 0, s, a, (int)per);
-  else launch_pdl(gn_apply_kernel<bf16, bf16>, dim3((unsigned)blocks), dim3(NT), 0, s, a, (int)per);
+  long long blocks = (ntok * nv + 512 * 4 - 1) / (512 * 4);
+  if (blocks > 148 * 2) blocks = 148 * 2;
+  if (blocks < 1) blocks = 1;
+  int lanes = (int)(blocks * 512 / nv);
+  if (lanes < 1) { lanes = 1; blocks = (nv + 511) / 512; }
+  if (a.x0.dtype == DT_F32) launch_pdl(gn_apply_wide_kernel<float, float>, dim3((unsigned)blocks), dim3(512), 0, s, a, lanes);
+  else launch_pdl(gn_apply_wide_kernel<bf16, bf16>, dim3((unsigned)blocks), dim3(512), 0, s, a, lanes);
 }
 
-void gn_init() {   // dynamic smem: ntl * nv * 32 floats <= 40 KB (C <= 2560)
-  cudaFuncSetAttribute(gn_stats_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  cudaFuncSetAttribute(gn_stats_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  cudaFuncSetAttribute(gn_fused_kernel<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  cudaFuncSetAttribute(gn_fused_kernel<bf16, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+void gn_init() {   // dynamic smem: ntl * nv * 32 floats <= 66 KB (ntl * nv <= 512)
+  cudaFuncSetAttribute(gn_stats_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  cudaFuncSetAttribute(gn_stats_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
 }
 
 }  // namespace pcpp

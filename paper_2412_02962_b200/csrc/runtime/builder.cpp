@@ -27,13 +27,14 @@ int band_rows(double p, int h) {
 
 pcpp_status validate(int H, int W, int C, int n, double p, int w, const pcpp_config* cfg) {
   if (!cfg) { set_error("cfg is NULL"); return PCPP_ERR_INVALID; }
-  if (cfg->model != PCPP_MODEL_TINY && cfg->model != PCPP_MODEL_SDXL) { set_error("unknown model %d", cfg->model); return PCPP_ERR_INVALID; }
-  const int levels = cfg->model == PCPP_MODEL_SDXL ? 3 : 1;
+  if (cfg->model < PCPP_MODEL_TINY || cfg->model > PCPP_MODEL_SDXL_XF) { set_error("unknown model %d", cfg->model); return PCPP_ERR_INVALID; }
+  const bool sdxl_like = cfg->model == PCPP_MODEL_SDXL || cfg->model == PCPP_MODEL_SDXL_XF;
+  const int levels = sdxl_like ? 3 : 1;
   const int div = 1 << (levels - 1);
   if (n < 1 || n > 8) { set_error("n_patches must be in [1, 8], got %d", n); return PCPP_ERR_INVALID; }
   if (C != 4) { set_error("latent channels must be 4, got %d", C); return PCPP_ERR_INVALID; }
   if (H <= 0 || W <= 0 || H % (n * div) != 0) { set_error("H=%d must be a positive multiple of n*%d=%d", H, div, n * div); return PCPP_ERR_INVALID; }
-  const int wq = cfg->model == PCPP_MODEL_SDXL ? 32 : 8;
+  const int wq = sdxl_like ? 32 : 8;
   if (W % wq != 0) { set_error("W=%d must be a multiple of %d", W, wq); return PCPP_ERR_INVALID; }
   if (!(p >= 0.0 && p <= 1.0)) { set_error("cond_fraction must be in [0, 1] (p > 1 undefined, P:209), got %g", p); return PCPP_ERR_INVALID; }
   if (cfg->num_steps < 1 || cfg->num_steps > 1000) { set_error("num_steps must be in [1, 1000]"); return PCPP_ERR_INVALID; }
@@ -49,6 +50,9 @@ pcpp_status validate(int H, int W, int C, int n, double p, int w, const pcpp_con
     if (cfg->world != n) { set_error("world (%d) must equal n_patches (%d)", cfg->world, n); return PCPP_ERR_INVALID; }
     if (cfg->rank < 0 || cfg->rank >= n) { set_error("rank out of range"); return PCPP_ERR_INVALID; }
     if (n > 1 && !cfg->nccl_id) { set_error("nccl_id required for the NCCL backend"); return PCPP_ERR_INVALID; }
+  } else if (cfg->comm_backend == PCPP_COMM_PEER) {
+    if (cfg->world != n) { set_error("world (%d) must equal n_patches (%d)", cfg->world, n); return PCPP_ERR_INVALID; }
+    if (cfg->rank < 0 || cfg->rank >= n) { set_error("rank out of range"); return PCPP_ERR_INVALID; }
   } else if (cfg->comm_backend != PCPP_COMM_LOOPBACK) { set_error("bad comm_backend"); return PCPP_ERR_INVALID; }
   return PCPP_OK;
 }
@@ -174,12 +178,14 @@ struct Builder {
     }
     for (int d = 0; d < depth; ++d) {
       std::string a = pre + ".attn" + std::to_string(d);
+      int tin = th;                          // the self-attention input: h, or LN1(h) in the _XF models
+      if (P.xf) tin = layernorm(th, a + ".ln1", level, C);
       long long wq = take(a + ".wq", {C, C}), wk = take(a + ".wk", {C, C}), wv = take(a + ".wv", {C, C});
       long long wo = take(a + ".wo", {C, C}), bo = take(a + ".bo", {C});
       int tq = tensor(a + ".q", level, C, act, 0, 0);
       int tkv = tensor(a + ".kv", level, 2 * C, act, 0, 1);
       {
-        Op& o = op(OP_GEMM); o.in0 = th; o.out = tq; o.out2 = tkv; o.n_split = C; o.N = 3 * C;
+        Op& o = op(OP_GEMM); o.in0 = tin; o.out = tq; o.out2 = tkv; o.n_split = C; o.N = 3 * C;
         o.w = up_mat(wq, (long long)C * C); up_mat(wk, (long long)C * C); up_mat(wv, (long long)C * C);
       }
       AttnX ax{}; ax.kv = tkv; ax.level = level; ax.h = rows_at(level); ax.W = w_at(level); ax.C = C;
@@ -192,6 +198,7 @@ struct Builder {
       int th2 = tensor(a + ".h", level, C, act, 0, 0);
       { Op& o = op(OP_GEMM); o.in0 = to; o.out = th2; o.N = C; o.w = up_mat(wo, (long long)C * C); o.b = up_f32(bo, C); o.res = th; }
       th = th2;
+      if (P.xf) th = xf_tail(th, a, level, C);
     }
     int tout = tensor(pre + ".out", level, C, act, out_pad ? 1 : 0, out_pad ? 1 : 0);
     long long w = take(pre + ".proj_out.w", {C, C}); long long b = take(pre + ".proj_out.b", {C});
@@ -199,11 +206,48 @@ struct Builder {
     return tout;
   }
 
+  // LayerNorm(C) of x into a new tensor (parameters <pre>.g, <pre>.b)
+  int layernorm(int x, const std::string& pre, int level, int C) {
+    int t = tensor(pre, level, C, act, 0, 0);
+    Op& o = op(OP_LN); o.in0 = x; o.out = t;
+    o.g = vec(pre + ".g", C); o.be = vec(pre + ".b", C);
+    return t;
+  }
+  // the rest of SDXL's transformer block after the self-attention (reading D25):
+  // h += W_xo CA(LN2 h, ctx) + b_xo;  h += W_ff2 (a * gelu(g)) + b_ff2, [a | g] = LN3(h) W_ff1 + b_ff1
+  int xf_tail(int th, const std::string& a, int level, int C) {
+    int tl2 = layernorm(th, a + ".ln2", level, C);
+    long long xq = take(a + ".xq", {C, C});
+    long long xk = take(a + ".xk", {C, P.ctx_dim}), xv = take(a + ".xv", {C, P.ctx_dim});
+    long long xo = take(a + ".xo", {C, C}), xbo = take(a + ".xbo", {C});
+    int tq = tensor(a + ".xq", level, C, act, 0, 0);
+    { Op& o = op(OP_GEMM); o.in0 = tl2; o.out = tq; o.N = C; o.w = up_mat(xq, (long long)C * C); }
+    XAttnX xa; xa.level = level; xa.C = C;
+    xa.w = up_mat(xk, (long long)C * P.ctx_dim); up_mat(xv, (long long)C * P.ctx_dim);   // [W_k; W_v] = [2C][ctx_dim]
+    P.xattns.push_back(xa);
+    int to = tensor(a + ".xo_in", level, C, act, 0, 0);
+    { Op& o = op(OP_XATTN); o.in0 = tq; o.out = to; o.xid = (int)P.xattns.size() - 1; }
+    int th2 = tensor(a + ".xh", level, C, act, 0, 0);
+    { Op& o = op(OP_GEMM); o.in0 = to; o.out = th2; o.N = C; o.w = up_mat(xo, (long long)C * C); o.b = up_f32(xbo, C); o.res = th; }
+    int tl3 = layernorm(th2, a + ".ln3", level, C);
+    long long f1 = take(a + ".ff1.w", {8 * C, C}), f1b = take(a + ".ff1.b", {8 * C});
+    long long f2 = take(a + ".ff2.w", {C, 4 * C}), f2b = take(a + ".ff2.b", {C});
+    int tu = tensor(a + ".ff_u", level, 8 * C, act, 0, 0);
+    { Op& o = op(OP_GEMM); o.in0 = tl3; o.out = tu; o.N = 8 * C; o.w = up_mat(f1, 8LL * C * C); o.b = up_f32(f1b, 8 * C); }
+    int tg = tensor(a + ".ff_g", level, 4 * C, act, 0, 0);
+    { Op& o = op(OP_GEGLU); o.in0 = tu; o.out = tg; }
+    int th3 = tensor(a + ".fh", level, C, act, 0, 0);
+    { Op& o = op(OP_GEMM); o.in0 = tg; o.out = th3; o.N = C; o.w = up_mat(f2, 4LL * C * C); o.b = up_f32(f2b, C); o.res = th2; }
+    return th3;
+  }
+
   struct TembRow { long long w, b; int cout, col; };
   std::vector<TembRow> temb_rows;
 
   void build(int model) {
-    const bool sdxl = model == PCPP_MODEL_SDXL;
+    const bool sdxl = model == PCPP_MODEL_SDXL || model == PCPP_MODEL_SDXL_XF;
+    P.xf = model == PCPP_MODEL_TINY_XF || model == PCPP_MODEL_SDXL_XF;
+    P.ctx_dim = P.xf ? (sdxl ? 2048 : 256) : 0;
     P.levels = sdxl ? 3 : 1; P.C0 = sdxl ? 320 : 128; P.T = 4 * P.C0; P.SIN = P.C0;
     long long w1 = take("time.lin1.w", {P.T, P.SIN}), b1 = take("time.lin1.b", {P.T});
     long long w2 = take("time.lin2.w", {P.T, P.T}), b2 = take("time.lin2.b", {P.T});

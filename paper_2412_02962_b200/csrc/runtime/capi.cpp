@@ -57,7 +57,7 @@ static Plan* manifest_plan(int model) {
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(model);
   if (it != cache.end()) return it->second.get();
-  if (model != PCPP_MODEL_TINY && model != PCPP_MODEL_SDXL) return nullptr;
+  if (model < PCPP_MODEL_TINY || model > PCPP_MODEL_SDXL_XF) return nullptr;
   auto P = std::make_unique<Plan>();
   pcpp_config_default(&P->cfg);
   P->cfg.model = model;
@@ -91,6 +91,7 @@ static void fill_info(Plan& P, pcpp_info* info) {
   info->n_conv = 0; info->n_gn = (int)P.gns.size(); info->n_attn = (int)P.attns.size();
   for (const Op& o : P.ops) if (o.k == OP_CONV || o.k == OP_CONVOUT) info->n_conv++;
   info->h_latent = P.H / P.n;
+  info->backend = P.backend;
   // activation bytes of one rank arena after the memory plan, and without it (every tensor its own range)
   if (!P.arena_tensor_bytes) plan_memory(P);
   info->arena_bytes_per_rank = (long long)P.arena_tensor_bytes;
@@ -151,6 +152,7 @@ static pcpp_status setup_plan(Plan& P, int H, int W, int C, int n, double p, int
   P.cfg = *cfg; P.H = H; P.W = W; P.C = C; P.n = n; P.p = p; P.warmup = w; P.S = cfg->num_steps;
   P.dtype = cfg->precision == PCPP_FP32 ? DT_F32 : DT_BF16;
   P.loopback = cfg->comm_backend == PCPP_COMM_LOOPBACK || n == 1;
+  P.backend = P.loopback ? PCPP_COMM_LOOPBACK : cfg->comm_backend;
   P.xasync = P.loopback && n > 1 && getenv("PCPP_LOOPBACK_ASYNC") && atoi(getenv("PCPP_LOOPBACK_ASYNC")) != 0;
   P.xdelay = (P.xasync && getenv("PCPP_XCH_DELAY")) ? atoll(getenv("PCPP_XCH_DELAY")) : 0;
   P.nr = P.loopback ? n : 1;
@@ -239,6 +241,7 @@ static pcpp_status step_internal(pcpp_plan_s* h, float* latent, int t) {
   Plan& P = *h->P;
   if (P.poisoned) { set_error("plan is poisoned by an earlier CUDA/NCCL error"); return PCPP_ERR_STATE; }
   if (t != P.k || t >= P.S) { set_error("pcpp_step(t=%d) but the plan is at step %d of %d", t, P.k, P.S); return PCPP_ERR_STATE; }
+  if (P.xf && !P.ctx_set) { set_error("_XF model: pcpp_set_context has not been called"); return PCPP_ERR_STATE; }
   const int sync = (P.n > 1 && (P.cfg.scheme == PCPP_SCHEME_SYNC || t < P.warmup)) ? 1 : 0;
   const int par = t & 1;
   const bool fork = (!P.loopback || P.xasync) && P.n > 1;
@@ -313,21 +316,40 @@ pcpp_status pcpp_set_cond(pcpp_plan_t h, const float* cond) {
   return PCPP_OK;
 }
 
+pcpp_status pcpp_set_context(pcpp_plan_t h, const float* ctx) {
+  GUARD_BEGIN
+  if (!h || !ctx) { set_error("NULL argument"); return PCPP_ERR_INVALID; }
+  Plan& P = *h->P;
+  if (!P.xf) { set_error("pcpp_set_context: the plan's model has no cross-attention (use an _XF model)"); return PCPP_ERR_INVALID; }
+  if (P.poisoned) { set_error("plan is poisoned"); return PCPP_ERR_STATE; }
+  pcpp_status st = context_setup(P, ctx);
+  if (st != PCPP_OK) P.poisoned = true;
+  return st;
+  GUARD_END
+}
+
 pcpp_status pcpp_sample(pcpp_plan_t h, const float* xT, const float* cond, float* x0) {
   GUARD_BEGIN
   if (!h || !xT || !cond || !x0) { set_error("NULL argument"); return PCPP_ERR_INVALID; }
   Plan& P = *h->P;
   const size_t patch = (size_t)(P.loopback ? P.H : P.H / P.n) * P.W * 4;
   const size_t full = (size_t)P.H * P.W * 4;
+  const bool peer = P.backend == PCPP_COMM_PEER;
+  if (peer && !P.peer_connected) { set_error("PEER backend: pcpp_peer_connect has not been called"); return PCPP_ERR_STATE; }
+  if (peer) h->lat_dev = reinterpret_cast<float*>(P.rm[0].arena + P.off_lat);   // the gather source lives in the arena
   if (!h->lat_dev) CKS(cudaMalloc(&h->lat_dev, patch * 4));
-  if (!P.loopback && !h->full_dev) CKS(cudaMalloc(&h->full_dev, full * 4));
+  if (!P.loopback && !peer && !h->full_dev) CKS(cudaMalloc(&h->full_dev, full * 4));
   pcpp_status st = pcpp_reset(h);
   if (st != PCPP_OK) return st;
   if ((st = pcpp_set_cond(h, cond)) != PCPP_OK) return st;
   CKS(cudaMemcpyAsync(h->lat_dev, xT, patch * 4, cudaMemcpyHostToDevice, P.s0));
   for (int k = 0; k < P.S; ++k) if ((st = step_internal(h, h->lat_dev, k)) != PCPP_OK) return st;
   const float* src = h->lat_dev;
-  if (!P.loopback) {
+  if (peer) {                  // push the patch into every rank's x0g, then a barrier
+    launch_copy_segments(P.push_dev + P.seg_x0.first, P.seg_x0.count, P.seg_x0.maxb, P.s0);
+    peer_barrier(P, P.s0);
+    src = reinterpret_cast<const float*>(P.rm[0].arena + P.off_x0g);
+  } else if (!P.loopback) {
     if (P.nccl->AllGather(h->lat_dev, h->full_dev, patch, nccl_float32, reinterpret_cast<ncclComm_t>(P.comm), P.s0) != 0) {
       set_error("final ncclAllGather failed"); return PCPP_ERR_NCCL;
     }
@@ -336,6 +358,27 @@ pcpp_status pcpp_sample(pcpp_plan_t h, const float* xT, const float* cond, float
   CKS(cudaMemcpyAsync(x0, src, full * 4, cudaMemcpyDeviceToHost, P.s0));
   CKS(cudaStreamSynchronize(P.s0));
   return PCPP_OK;
+  GUARD_END
+}
+
+pcpp_status pcpp_peer_handle(pcpp_plan_t h, void* out64) {
+  GUARD_BEGIN
+  if (!h || !out64) { set_error("NULL argument"); return PCPP_ERR_INVALID; }
+  Plan& P = *h->P;
+  if (P.backend != PCPP_COMM_PEER) { set_error("pcpp_peer_handle: plan does not use the PEER backend"); return PCPP_ERR_STATE; }
+  cudaIpcMemHandle_t mh;
+  CKS(cudaIpcGetMemHandle(&mh, P.rm[0].arena));
+  std::memcpy(out64, &mh, sizeof mh);
+  return PCPP_OK;
+  GUARD_END
+}
+
+pcpp_status pcpp_peer_connect(pcpp_plan_t h, const void* handles) {
+  GUARD_BEGIN
+  if (!h || !handles) { set_error("NULL argument"); return PCPP_ERR_INVALID; }
+  pcpp_status st = plan_peer_connect(*h->P, handles);
+  if (st == PCPP_ERR_CUDA) h->P->poisoned = true;
+  return st;
   GUARD_END
 }
 
@@ -350,6 +393,8 @@ pcpp_status pcpp_query(pcpp_plan_t h, pcpp_info* info) {
   info->device_bytes = (long long)P.rank_bytes * P.nr + (long long)P.wmat_len * (long long)dtype_size(P.dtype) + P.wf32_len * 4;
   info->graphs = P.cfg.use_graphs;
   info->tc_kernels = P.use_tc;
+  info->simt_fallbacks = P.simt_fallbacks;
+  std::snprintf(info->comm_lib, sizeof info->comm_lib, "%s", P.backend == PCPP_COMM_NCCL ? comm_lib_path() : "");
   return PCPP_OK;
   GUARD_END
 }
@@ -409,7 +454,12 @@ pcpp_status pcpp_debug_comm_off(pcpp_plan_t h, int on) {
 void pcpp_destroy(pcpp_plan_t h) {
   if (!h) return;
   if (h->P && h->P->s0) cudaStreamSynchronize(h->P->s0);
-  if (h->lat_dev) cudaFree(h->lat_dev);
+  if (h->P && h->P->backend == PCPP_COMM_PEER && h->P->peer_connected && !h->P->poisoned) {
+    // collective: no peer may still push into this arena when it is unmapped and freed
+    peer_barrier(*h->P, h->P->s0);
+    cudaStreamSynchronize(h->P->s0);
+  }
+  if (h->lat_dev && !(h->P && h->P->backend == PCPP_COMM_PEER)) cudaFree(h->lat_dev);
   if (h->full_dev) cudaFree(h->full_dev);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
@@ -499,9 +549,9 @@ pcpp_status pcpp_op_groupnorm(const void* x, int rows, int B, int W, int C, cons
   GnStatsArgs a;
   a.x0.base = const_cast<void*>(x); a.x0.rows = rows; a.x0.B = B; a.x0.W = W; a.x0.C = C; a.x0.dtype = dt;
   a.c0 = C; a.C = C; a.nchunk = gn_stats_chunks(rows, W);
-  char* sc = reinterpret_cast<char*>(op_scratch(WS_GN, (size_t)B * a.nchunk * 32 * 2 * 8 + 256, true));
+  char* sc = reinterpret_cast<char*>(op_scratch(WS_GN, (size_t)a.nchunk * 128 * 8, true));
   if (!sc) { set_error("scratch alloc"); return PCPP_ERR_OOM; }
-  a.counter = reinterpret_cast<unsigned*>(sc); a.partial = reinterpret_cast<double*>(sc + 256);
+  a.partial = reinterpret_cast<double*>(sc);
   a.m_out = m_out;
   launch_gn_stats(a, s);
   GnApplyArgs p;

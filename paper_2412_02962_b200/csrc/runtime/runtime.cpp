@@ -20,27 +20,42 @@ namespace pcpp {
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { set_error("CUDA %s at %s:%d: %s", #x, __FILE__, __LINE__, cudaGetErrorString(e_)); return PCPP_ERR_CUDA; } } while (0)
 
+static char g_comm_lib[512] = "";
+const char* comm_lib_path() { return g_comm_lib; }
+
+// libnccl is dlopen'd: PCPP_NCCL_LIB (the Python binding sets it to the NCCL that torch ships) or,
+// failing that, the loader's libnccl.so.2 (an NCCL already loaded by the process is reused)
 NcclApi* nccl_api() {
   static NcclApi api;
   static bool tried = false;
   if (api.handle) return &api;
   if (tried) { set_error("NCCL could not be loaded"); return nullptr; }
   tried = true;
-  const char* cands[] = {"libnccl.so.2",
-                         "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
-  for (const char* c : cands) { api.handle = dlopen(c, RTLD_NOW | RTLD_GLOBAL); if (api.handle) break; }
-  if (!api.handle) { set_error("dlopen(libnccl.so.2) failed"); return nullptr; }
+  const char* env = getenv("PCPP_NCCL_LIB");
+  const char* cands[] = {env && *env ? env : nullptr, "libnccl.so.2"};
+  for (const char* c : cands) {
+    if (!c) continue;
+    api.handle = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+    if (api.handle) break;
+  }
+  if (!api.handle) { set_error("dlopen(libnccl.so.2) failed (set PCPP_NCCL_LIB)"); return nullptr; }
 #define SYM(f, n) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.handle, n)); if (!api.f) { set_error("missing %s", n); api.handle = nullptr; return nullptr; }
   SYM(GetUniqueId, "ncclGetUniqueId"); SYM(CommInitRank, "ncclCommInitRank"); SYM(CommDestroy, "ncclCommDestroy");
   SYM(CommAbort, "ncclCommAbort"); SYM(Send, "ncclSend"); SYM(Recv, "ncclRecv"); SYM(AllGather, "ncclAllGather");
   SYM(GroupStart, "ncclGroupStart"); SYM(GroupEnd, "ncclGroupEnd"); SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
+  Dl_info di;
+  if (dladdr(reinterpret_cast<void*>(api.GetUniqueId), &di) && di.dli_fname)
+    snprintf(g_comm_lib, sizeof g_comm_lib, "%s", di.dli_fname);
   return &api;
 }
 
 Plan::~Plan() {
   for (auto& g : graphs) for (auto& x : g) if (x) cudaGraphExecDestroy(x);
   if (comm && nccl) nccl->CommDestroy(reinterpret_cast<ncclComm_t>(comm));
+  for (int j = 0; j < 8; ++j)
+    if (peer_base[j] && (rm.empty() || peer_base[j] != rm[0].arena)) cudaIpcCloseMemHandle(peer_base[j]);
+  if (push_dev) cudaFree(push_dev);
   for (auto& r : rm) if (r.arena) cudaFree(r.arena);
   for (void* p : gallocs) cudaFree(p);
   if (segs_dev) cudaFree(segs_dev);
@@ -70,8 +85,7 @@ size_t plan_memory(Plan& P) {
       if (r >= 0) { first[r] = std::min(first[r], i); last[r] = std::max(last[r], i); }
   }
   std::vector<char> pinned(nt, 0);
-  static const int plan_env = getenv("PCPP_MEMPLAN") ? atoi(getenv("PCPP_MEMPLAN")) : 1;
-  for (int t = 0; t < nt; ++t) pinned[t] = !plan_env || P.td[t].dbl || P.td[t].pad || last[t] < 0;
+  for (int t = 0; t < nt; ++t) pinned[t] = P.td[t].dbl || P.td[t].pad || last[t] < 0;
   for (const HaloX& h : P.halos) pinned[h.t] = 1;
   for (const AttnX& a : P.attns) pinned[a.kv] = 1;
   size_t off = 0;
@@ -120,15 +134,13 @@ pcpp_status plan_allocate(Plan& P) {
   for (auto& g : P.gns) {
     for (int q = 0; q < 2; ++q) { g.off_m[q] = off; off = align256(off + mb); }
     for (int q = 0; q < 2; ++q) { g.off_mall[q] = off; off = align256(off + mb * P.n); }
-    g.off_part = off; off = align256(off + (size_t)B_CFG * g.nchunk * GN_G * 2 * sizeof(double));
-    g.off_cnt = off; off = align256(off + 16);
+    g.off_part = off; off = align256(off + (size_t)g.nchunk * 128 * sizeof(double));
   }
   // GN statistics fused into the producing GEMM's epilogue (bf16 tensor-core path): the GN reads
   // x0 only, and x0's last writer is a CONV/GEMM that writes nothing else
-  static const int gn_fuse_env = getenv("PCPP_GN_FUSE") ? atoi(getenv("PCPP_GN_FUSE")) : 1;
   for (size_t i = 0; i < P.ops.size(); ++i) {
     Op& o = P.ops[i];
-    if (o.k != OP_GN || o.in1 >= 0 || !gn_fuse_env || P.dtype != DT_BF16) continue;
+    if (o.k != OP_GN || o.in1 >= 0 || P.dtype != DT_BF16) continue;
     for (size_t j = i; j-- > 0;) {
       Op& pr = P.ops[j];
       if (pr.out != o.in0 && pr.out2 != o.in0) continue;
@@ -136,7 +148,7 @@ pcpp_status plan_allocate(Plan& P) {
       break;
     }
   }
-  P.off_epart = off; off = align256(off + (size_t)148 * 4 * 128 * sizeof(float));
+  P.off_epart = off; off = align256(off + (size_t)148 * 4 * 128 * sizeof(double));
   P.gn_slots.assign((size_t)P.nr * P.gns.size(), 0);
   const size_t es = dtype_size(P.dtype);
   size_t gat_level[3] = {0, 0, 0};
@@ -156,6 +168,11 @@ pcpp_status plan_allocate(Plan& P) {
         a.off_gat[0] = a.off_gat[1] = gat_level[a.level];
       }
     }
+  }
+  if (P.backend == PCPP_COMM_PEER) {    // flags [n] + epoch, gathered x_0, the latent patch (pcpp_sample)
+    P.off_sig = off; off = align256(off + 16 * sizeof(unsigned long long));
+    P.off_x0g = off; off = align256(off + (size_t)P.H * P.W * 4 * sizeof(float));
+    P.off_lat = off; off = align256(off + (size_t)(P.H / P.n) * P.W * 4 * sizeof(float));
   }
   P.rank_bytes = off;
   P.rm.resize(P.nr);
@@ -190,6 +207,12 @@ pcpp_status plan_allocate(Plan& P) {
       }
     P.ws_elems = std::min<size_t>(8 * mx, (size_t)1 << 28);
     P.ws = (float*)galloc(P.ws_elems * 4);
+  }
+  if (P.xf) {     // cross-attention context: as given, laid out per level, and every layer's keys/values
+    P.ctx_f32 = (float*)galloc((size_t)2 * 77 * P.ctx_dim * 4);
+    for (int l = 0; l < P.levels; ++l)
+      P.ctx_level[l] = galloc((size_t)P.ctx_rows(l) * B_CFG * (P.W >> l) * P.ctx_dim * es);
+    for (auto& xa : P.xattns) xa.kv = galloc((size_t)P.ctx_rows(xa.level) * B_CFG * (P.W >> xa.level) * 2 * xa.C * es);
   }
   for (void* p : P.gallocs) if (!p) { set_error("cudaMalloc failed for global buffers"); return PCPP_ERR_OOM; }
   // DDIM schedule (reading D2): scaled_linear betas, 'leading' spacing, offset 1, final ab_prev = ab[0]
@@ -456,7 +479,7 @@ void compute_ledgers(Plan& P, pcpp_info* info) {
 // NCCL
 // ---------------------------------------------------------------------------------------------
 pcpp_status plan_init_comm(Plan& P) {
-  if (P.loopback || P.n == 1) return PCPP_OK;
+  if (P.loopback || P.n == 1 || P.backend == PCPP_COMM_PEER) return PCPP_OK;
   P.nccl = nccl_api();
   if (!P.nccl) return PCPP_ERR_NCCL;
   ncclUniqueId id; std::memcpy(&id, P.cfg.nccl_id, sizeof id);
@@ -464,6 +487,61 @@ pcpp_status plan_init_comm(Plan& P) {
   ncclResult_t r = P.nccl->CommInitRank(&c, P.n, id, P.cfg.rank);
   if (r != 0) { set_error("ncclCommInitRank: %s", P.nccl->GetErrorString(r)); return PCPP_ERR_NCCL; }
   P.comm = c;
+  return PCPP_OK;
+}
+
+void peer_barrier(Plan& P, cudaStream_t s) { launch_peer_barrier(P.bar, s); }
+
+// Open every peer's arena (IPC handles in rank order, from pcpp_peer_handle on each rank) and build
+// this rank's push lists: the loopback transfer list of every exchange point restricted to
+// src == me, source in the own arena, destination at the same offset in the peer's arena (every
+// rank's plan has the same layout).
+pcpp_status plan_peer_connect(Plan& P, const void* handles) {
+  if (P.backend != PCPP_COMM_PEER) { set_error("pcpp_peer_connect: plan does not use the PEER backend"); return PCPP_ERR_STATE; }
+  if (P.peer_connected) { set_error("pcpp_peer_connect: already connected"); return PCPP_ERR_STATE; }
+  const int me = P.rank0, n = P.n;
+  char* own = P.rm[0].arena;
+  const cudaIpcMemHandle_t* hs = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int j = 0; j < n; ++j) {
+    if (j == me) { P.peer_base[j] = own; continue; }
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, hs[j], cudaIpcMemLazyEnablePeerAccess));
+    P.peer_base[j] = reinterpret_cast<char*>(ptr);
+  }
+  auto remote = [&](int rank, const BufRef& r) { return P.peer_base[rank] + (resolve(P, 0, r) - own); };
+  std::vector<CopySeg> host;
+  std::vector<Xfer> lb;
+  for (int sync = 0; sync < 2; ++sync)
+    for (int par = 0; par < 2; ++par) {
+      P.seg_push[sync][par].assign(P.xg[sync][par].size(), Plan::SegRange{});
+      for (size_t i = 0; i < P.ops.size(); ++i) {
+        const int xo = P.op_xord[i];
+        if (xo < 0) continue;
+        make_group(P, P.ops[i], sync, par, lb);
+        Plan::SegRange sr; sr.first = (int)host.size();
+        for (const Xfer& x : lb) {
+          if (x.src_rank != me) continue;
+          host.push_back(CopySeg{resolve(P, 0, x.src), remote(x.dst_rank, x.dst), (unsigned long long)x.bytes});
+          sr.maxb = std::max<unsigned long long>(sr.maxb, x.bytes);
+        }
+        sr.count = (int)host.size() - sr.first;
+        P.seg_push[sync][par][xo] = sr;
+      }
+    }
+  {   // final gather: my latent patch into row block `me` of every rank's x0g
+    const size_t pb = (size_t)(P.H / n) * P.W * 4 * sizeof(float);
+    P.seg_x0.first = (int)host.size();
+    for (int j = 0; j < n; ++j)
+      host.push_back(CopySeg{own + P.off_lat, P.peer_base[j] + P.off_x0g + (size_t)me * pb, (unsigned long long)pb});
+    P.seg_x0.count = n; P.seg_x0.maxb = pb;
+  }
+  CK(cudaMalloc(&P.push_dev, std::max<size_t>(1, host.size()) * sizeof(CopySeg)));
+  CK(cudaMemcpy(P.push_dev, host.data(), host.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
+  P.bar.n = n; P.bar.me = me;
+  P.bar.flags = reinterpret_cast<const unsigned long long*>(own + P.off_sig);
+  P.bar.epoch = reinterpret_cast<unsigned long long*>(own + P.off_sig) + 8;
+  for (int j = 0; j < n; ++j) P.bar.remote[j] = reinterpret_cast<unsigned long long*>(P.peer_base[j] + P.off_sig) + me;
+  P.peer_connected = true;
   return PCPP_OK;
 }
 
@@ -488,6 +566,26 @@ static pcpp_status exchange(Plan& P, int xo, int sync, int par) {
     const auto& sr = P.seg_remote[sync][par][xo];
     launch_copy_segments(P.segs_dev + sr.first, sr.count, sr.maxb, P.s0);
     P.launches_per_step += sr.count > 0;
+    return PCPP_OK;
+  }
+  if (P.backend == PCPP_COMM_PEER) {
+    // one-sided pushes of this rank's data into the peers' buffers (the loopback transfer list
+    // restricted to src == me).  Async: on the comm stream behind the producer, consumed one step
+    // later (the step-start barrier orders it).  Warm-up: on the compute stream, then a barrier;
+    // an all-gather of attention K/V first waits until every peer has left the previous attention
+    // layer (the gather buffer is shared by the layers of a level).
+    const auto& sr = P.seg_push[sync][par][xo];
+    if (!sync) {
+      CK(cudaEventRecord(P.ev_x, P.s0));
+      CK(cudaStreamWaitEvent(P.s1, P.ev_x, 0));
+      launch_copy_segments(P.push_dev + sr.first, sr.count, sr.maxb, P.s1);
+      P.launches_per_step += sr.count > 0;
+    } else {
+      if (G.allgather && G.cls == 0) { peer_barrier(P, P.s0); P.launches_per_step += 1; }
+      launch_copy_segments(P.push_dev + sr.first, sr.count, sr.maxb, P.s0);
+      peer_barrier(P, P.s0);
+      P.launches_per_step += (sr.count > 0) + 1;
+    }
     return PCPP_OK;
   }
   ncclComm_t comm = reinterpret_cast<ncclComm_t>(P.comm);
@@ -543,6 +641,7 @@ static unsigned op_kind(OpK k) {
     case OP_ATTN: return K_ATTN;
     case OP_GN: return K_GN;
     case OP_HALO: case OP_KVX: return K_XCH;
+    case OP_XATTN: return K_ATTN;
     case OP_END: return K_END;
     default: return K_MISC;
   }
@@ -583,7 +682,7 @@ pcpp_status plan_autotune(Plan& P) {
     if (op.out2 >= 0) { g.out2 = view(P, 0, op.out2, 0); g.n_split = op.n_split; }
     g.ws = P.ws; g.ws_elems = P.ws_elems;
     int slots = 0;
-    if (op.gn_fuse >= 0) { g.gn_part = reinterpret_cast<float*>(P.rm[0].arena + P.off_epart); g.gn_slots = &slots; }
+    if (op.gn_fuse >= 0) { g.gn_part = reinterpret_cast<double*>(P.rm[0].arena + P.off_epart); g.gn_slots = &slots; }
     if (gemm_tc_supported(g)) gemm_tc_autotune(g, P.s0);
   }
   if (getenv("PCPP_TUNE_SAVE")) gemm_tune_save(getenv("PCPP_TUNE_SAVE"));
@@ -592,10 +691,45 @@ pcpp_status plan_autotune(Plan& P) {
   return PCPP_OK;
 }
 
+// _XF models: lay the context out per level and compute every layer's context keys/values
+// [ctx W_k ; ctx W_v] with the plan's GEMM kernels (once per context; reading D26)
+pcpp_status context_setup(Plan& P, const float* ctx_host) {
+  const size_t es = dtype_size(P.dtype);
+  CK(cudaMemcpyAsync(P.ctx_f32, ctx_host, (size_t)2 * 77 * P.ctx_dim * 4, cudaMemcpyHostToDevice, P.s0));
+  for (int l = 0; l < P.levels; ++l) {
+    ActView v; v.base = P.ctx_level[l]; v.rows = P.ctx_rows(l); v.B = B_CFG; v.W = P.W >> l; v.C = P.ctx_dim; v.dtype = P.dtype;
+    launch_ctx_layout(P.ctx_f32, v, 77, P.s0);
+  }
+  const char* wm = reinterpret_cast<const char*>(P.wmat);
+  for (const XAttnX& xa : P.xattns) {
+    GemmArgs g;
+    g.a0.base = P.ctx_level[xa.level]; g.a0.rows = P.ctx_rows(xa.level); g.a0.B = B_CFG; g.a0.W = P.W >> xa.level;
+    g.a0.C = P.ctx_dim; g.a0.dtype = P.dtype;
+    g.c0 = g.cin = P.ctx_dim; g.taps = 1; g.stride = 1;
+    g.rows_out = g.a0.rows; g.w_out = g.a0.W; g.B = B_CFG;
+    g.w = wm + (size_t)xa.w * es; g.wdtype = P.dtype; g.N = 2 * xa.C;
+    g.out = g.a0; g.out.base = xa.kv; g.out.C = 2 * xa.C;
+    g.ws = P.ws; g.ws_elems = P.ws_elems;
+    launch_gemm_tc_or_simt(P, g, P.s0);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(P.s0));
+  P.ctx_set = true;
+  return PCPP_OK;
+}
+
 pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
   const int n = P.n, nr = P.nr;
   cudaStream_t s = P.s0;
   P.launches_per_step = 0;
+  const long long fb0 = simt_fallback_count();
+  // PEER: every peer has finished step k-1 (its compute and its pushes) before this step reads what
+  // they pushed during k-1 and before this step pushes into the buffers they read during k-1
+  if (P.backend == PCPP_COMM_PEER && n > 1 && (mask & K_XCH)) {
+    if (!P.peer_connected) { set_error("PEER backend: pcpp_peer_connect has not been called"); return PCPP_ERR_STATE; }
+    peer_barrier(P, s);
+    P.launches_per_step += 1;
+  }
   const size_t es = dtype_size(P.dtype);
   const char* wm = reinterpret_cast<const char*>(P.wmat);
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
@@ -648,7 +782,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           if (op.out2 >= 0) { g.out2 = view(P, vr, op.out2, par); g.n_split = op.n_split; }
           g.ws = P.ws; g.ws_elems = P.ws_elems;
           if (op.gn_fuse >= 0) {
-            g.gn_part = reinterpret_cast<float*>(P.rm[vr].arena + P.off_epart);
+            g.gn_part = reinterpret_cast<double*>(P.rm[vr].arena + P.off_epart);
             g.gn_slots = &P.gn_slots[(size_t)vr * P.gns.size() + op.gn_fuse];
           }
           launch_gemm_tc_or_simt(P, g, s);
@@ -663,7 +797,6 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           if (op.in1 >= 0) a.x1 = view(P, vr, op.in1, par);
           char* base = P.rm[vr].arena;
           a.partial = reinterpret_cast<double*>(base + gx.off_part);
-          a.counter = reinterpret_cast<unsigned*>(base + gx.off_cnt);
           a.m_out = reinterpret_cast<double*>(base + gx.off_m[par]);
           a.nchunk = gx.nchunk;
           return a;
@@ -690,7 +823,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           for (int vr = 0; vr < nr && do_op; ++vr) {
             const int slots = P.gn_slots[(size_t)vr * P.gns.size() + op.xid];
             if (slots > 0)
-              launch_gn_finalize(reinterpret_cast<const float*>(P.rm[vr].arena + P.off_epart), slots,
+              launch_gn_finalize(reinterpret_cast<const double*>(P.rm[vr].arena + P.off_epart), slots,
                                  reinterpret_cast<double*>(P.rm[vr].arena + gx.off_m[par]), s);
             else
               launch_gn_stats(stats_args(vr), s);
@@ -735,6 +868,32 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
         P.launches_per_step += nr;
         break;
       }
+      case OP_LN:
+        for (int vr = 0; vr < nr; ++vr)
+          if (!launch_layernorm(view(P, vr, op.in0, par), view(P, vr, op.out, par), P.wf32 + op.g, P.wf32 + op.be, s)) {
+            set_error("LayerNorm: unsupported channel count %d", P.td[op.in0].C); return PCPP_ERR_UNSUPPORTED;
+          }
+        P.launches_per_step += nr;
+        break;
+      case OP_GEGLU:
+        for (int vr = 0; vr < nr; ++vr) launch_geglu(view(P, vr, op.in0, par), view(P, vr, op.out, par), s);
+        P.launches_per_step += nr;
+        break;
+      case OP_XATTN: {     // cross-attention: queries of the patch, keys/values of the 77-token context
+        const XAttnX& xa = P.xattns[op.xid];
+        for (int vr = 0; vr < nr; ++vr) {
+          const ActView q = view(P, vr, op.in0, par);
+          AttnArgs a;
+          a.q = q.base; a.h = q.rows; a.B = B_CFG; a.W = q.W; a.C = xa.C; a.dtype = P.dtype;
+          a.out = view(P, vr, op.out, par).base;
+          a.src[0] = AttnSrc{xa.kv, P.ctx_rows(xa.level), 77};
+          a.nsrc = 1;
+          a.ws = P.ws; a.ws_elems = P.ws_elems;
+          launch_attn_tc_or_simt(P, a, s);
+        }
+        P.launches_per_step += nr;
+        break;
+      }
       case OP_UPS:
         for (int vr = 0; vr < nr; ++vr) launch_upsample2(view(P, vr, op.in0, par), view(P, vr, op.out, par), s);
         P.launches_per_step += nr;
@@ -768,18 +927,20 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
     }
   }
   if (P.op_ev_on) cudaEventRecord(P.op_ev[P.ops.size()], s);
+  P.simt_fallbacks = std::max<int>(P.simt_fallbacks, (int)(simt_fallback_count() - fb0));
   CK(cudaGetLastError());
   return PCPP_OK;
 }
 
 // Per-op device time of one eager step (events between ops; the host runs ahead of the device for
-// every op longer than the launch latency), printed to stderr.  Debug / tuning aid only.
+// every op longer than the launch latency), printed to stderr.  Debug / tuning aid only.  The
+// step-end op (device step counter) is excluded, so the plan's step bookkeeping is unchanged.
 void print_op_timing(Plan& P, float* latent, int sync, int par) {
   const size_t n = P.ops.size() + 1;
   P.op_ev.resize(n);
   for (auto& e : P.op_ev) cudaEventCreate(&e);
   P.op_ev_on = true;
-  for (int rep = 0; rep < 2; ++rep) run_step(P, latent, sync, par, ~0u);
+  for (int rep = 0; rep < 2; ++rep) run_step(P, latent, sync, par, K_ALL & ~K_END);   // k_dev untouched
   cudaStreamSynchronize(P.s0);
   P.op_ev_on = false;
   static const char* names[] = {"TEMB", "PREP", "HALO", "CONV", "GEMM", "GN", "KVX", "ATTN", "UPS", "COUT", "CFG", "END"};
@@ -834,6 +995,14 @@ void op_work(const Plan& P, unsigned kind, int sync, double* flops, double* byte
           f += 4.0 * ((double)a.h * a.W) * ((double)kv * a.W) * a.C * B_CFG;
           by += ((double)a.h * a.W * a.C * 2 + (double)kv * a.W * 2 * a.C) * B_CFG * es;   // Q + O + K/V
         }
+        nl += P.nr;
+        break;
+      }
+      case OP_XATTN: {
+        const XAttnX& xa = P.xattns[op.xid];
+        const TDesc& q = P.td[op.in0];
+        f += 4.0 * ((double)q.rows * q.W) * 77.0 * xa.C * B_CFG * P.nr;
+        by += ((double)q.rows * q.W * xa.C * 2 + 77.0 * 2 * xa.C) * B_CFG * es * P.nr;
         nl += P.nr;
         break;
       }

@@ -26,7 +26,7 @@ struct TDesc {
 
 // ---- ops ------------------------------------------------------------------------------------------
 enum OpK { OP_TEMB, OP_PREP, OP_HALO, OP_CONV, OP_GEMM, OP_GN, OP_KVX, OP_ATTN, OP_UPS, OP_CONVOUT,
-           OP_CFGDDIM, OP_END };
+           OP_CFGDDIM, OP_END, OP_LN, OP_GEGLU, OP_XATTN };
 
 struct Op {
   OpK k;
@@ -44,8 +44,11 @@ struct Op {
 
 // ---- exchange buffers --------------------------------------------------------------------------
 struct HaloX { int t; int stride; };
-struct GnX   { int C; int rows, W; size_t off_m[2], off_mall[2], off_part, off_cnt; int nchunk; double count; };
+struct GnX   { int C; int rows, W; size_t off_m[2], off_mall[2], off_part; int nchunk; double count; };
 struct AttnX { int kv; int level; int h, W, C; int r; size_t off_top[2], off_bot[2]; size_t off_gat[2]; };
+// cross-attention of an _XF layer: keys/values of the context, [ctx_rows(level)][B][W_l][2C] (global,
+// shared by the virtual ranks), produced at pcpp_set_context by a GEMM of the level's laid-out context
+struct XAttnX { int level, C; long long w; void* kv = nullptr; };
 
 // A symbolic buffer reference, resolved per rank to a device pointer.
 enum BufKind { BK_TENSOR, BK_TOP, BK_BOT, BK_GAT, BK_GNM, BK_GNMALL };
@@ -91,6 +94,11 @@ struct Plan {
   std::vector<HaloX> halos;
   std::vector<GnX> gns;
   std::vector<AttnX> attns;
+  std::vector<XAttnX> xattns;
+  bool xf = false; int ctx_dim = 0; bool ctx_set = false;
+  float* ctx_f32 = nullptr;                 // [2][77][ctx_dim] as given
+  void* ctx_level[3] = {nullptr, nullptr, nullptr};   // laid-out context per level [ctx_rows][2][W_l][ctx_dim]
+  int ctx_rows(int level) const { const int Wl = W >> level; return (77 + Wl - 1) / Wl; }
   int J = 0;             // total temb projection width (sum of ResBlock Cout)
   // manifest
   std::vector<std::string> man_name;
@@ -139,6 +147,18 @@ struct Plan {
   NcclApi* nccl = nullptr;
   void* comm = nullptr;   // ncclComm_t
 
+  // PEER backend (PCPP_COMM_PEER): exchanges are one-sided pushes into the peers' arenas (CUDA IPC
+  // mappings; NVLink stores across GPUs) + device flag barriers (kernels/peer.cu)
+  int backend = PCPP_COMM_LOOPBACK;     // effective backend (n == 1 runs LOOPBACK)
+  bool peer_connected = false;
+  char* peer_base[8] = {};              // every rank's arena in this address space (own at [rank0])
+  size_t off_sig = 0, off_x0g = 0, off_lat = 0;   // flags + epoch; gathered x_0 [H][W][4]; latent patch [h][W][4]
+  PeerBarrier bar;
+  std::vector<SegRange> seg_push[2][2]; // [sync][par] per exchange ordinal: this rank's pushes
+  SegRange seg_x0;                      // final gather of x_0 into every rank's x0g
+  CopySeg* push_dev = nullptr;
+  int simt_fallbacks = 0;               // launches of a captured step that fell back from tcgen05 to SIMT
+
   ~Plan();
 };
 
@@ -152,12 +172,17 @@ pcpp_status plan_allocate(Plan& P);
 pcpp_status plan_upload_weights(Plan& P, const float* blob);
 pcpp_status plan_build_exchanges(Plan& P);
 pcpp_status plan_init_comm(Plan& P);
+pcpp_status plan_peer_connect(Plan& P, const void* handles);
+void peer_barrier(Plan& P, cudaStream_t s);
+const char* comm_lib_path();
 pcpp_status plan_autotune(Plan& P);
 enum { K_GEMM = 1, K_ATTN = 2, K_GN = 4, K_XCH = 8, K_MISC = 16, K_END = 32, K_ALL = 63 };
 pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask = K_ALL);
+pcpp_status context_setup(Plan& P, const float* ctx_host);
 // algorithmic work of the ops of one kind in one step (all virtual ranks): flops, bytes, launches
 void op_work(const Plan& P, unsigned kind, int sync, double* flops, double* bytes, int* launches);
 int band_rows(double p, int h);
+long long simt_fallback_count();
 void print_op_timing(Plan& P, float* latent, int sync, int par);
 const char* set_error(const char* fmt, ...);
 

@@ -22,6 +22,7 @@ import numpy as np
 SEED_WEIGHTS = 0
 SEED_XT = 1
 SEED_COND = 2
+SEED_CONTEXT = 3
 
 
 def init_specs(manifest) -> list[tuple[int, float, float]]:
@@ -49,7 +50,7 @@ def init_specs(manifest) -> list[tuple[int, float, float]]:
             out.append((numel, 0.0, float(std)))
         elif len(shape) == 2:
             std = 1.0 / np.sqrt(shape[1])
-            if leaf == "wo":
+            if leaf in ("wo", "xo") or name.endswith(".ff2.w"):     # residual-branch outputs of a block
                 std /= np.sqrt(2.0 * depth[name[: name.rindex(".attn")]])
             elif name.endswith("proj_out.w"):
                 std /= np.sqrt(2.0)
@@ -98,15 +99,26 @@ def round_to_bf16(a: np.ndarray) -> np.ndarray:
     that bf16-mode parity runs feed both sides identical (pre-rounded) weights.
     """
     a = np.ascontiguousarray(a, dtype=np.float32)
-    u = a.view(np.uint32).astype(np.uint64)
-    lsb = (u >> 16) & 1
-    u = (u + 0x7FFF + lsb) & 0xFFFF0000
-    return u.astype(np.uint32).view(np.float32)
+    out = np.empty_like(a)
+    src, dst = a.reshape(-1).view(np.uint32), out.reshape(-1).view(np.uint32)
+    step = 1 << 24                      # chunked: the SDXL_XF blob has 2.6 G values
+    for i in range(0, src.size, step):
+        u = src[i:i + step].astype(np.uint64)
+        lsb = (u >> 16) & 1
+        dst[i:i + step] = ((u + 0x7FFF + lsb) & 0xFFFF0000).astype(np.uint32)
+    return out
 
 
 def make_latent(H: int, W: int, C: int = 4, seed: int = SEED_XT) -> np.ndarray:
     """x_T ~ N(0, I) as [H, W, C] float32 (row-major, C innermost)."""
     z = np.random.Generator(np.random.PCG64(seed)).standard_normal((H, W, C))
+    return z.astype(np.float32)
+
+
+def make_context(ctx_len: int, dim: int, seed: int = SEED_CONTEXT) -> np.ndarray:
+    """Cross-attention context of the '_xf' models (reading D26): [2, ctx_len, dim] float32 ~ N(0, I);
+    [0] = the unconditional branch's (SDXL encodes the empty prompt: not zeros), [1] = the prompt's."""
+    z = np.random.Generator(np.random.PCG64(seed)).standard_normal((2, ctx_len, dim))
     return z.astype(np.float32)
 
 

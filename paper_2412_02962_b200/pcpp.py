@@ -14,11 +14,14 @@ LIB_PATH = os.path.join(HERE, "libpcpp.so")
 OK, ERR_INVALID, ERR_STATE, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_UNSUPPORTED = range(7)
 FP32, BF16 = 0, 1
 SCHEME_PCPP, SCHEME_FULLMAP, SCHEME_SYNC = 0, 1, 2
-MODEL_TINY, MODEL_SDXL = 0, 1
-COMM_NCCL, COMM_LOOPBACK = 0, 1
+MODEL_TINY, MODEL_SDXL, MODEL_TINY_XF, MODEL_SDXL_XF = 0, 1, 2, 3
+CTX_LEN = 77
+COMM_NCCL, COMM_LOOPBACK, COMM_PEER = 0, 1, 2
+BACKENDS = {"nccl": COMM_NCCL, "loopback": COMM_LOOPBACK, "peer": COMM_PEER}
+PEER_HANDLE_BYTES = 64
 KERNELS_AUTO, KERNELS_SIMT = 0, 1
 MAX_LAYERS = 128
-MODELS = {"tiny": MODEL_TINY, "sdxl": MODEL_SDXL}
+MODELS = {"tiny": MODEL_TINY, "sdxl": MODEL_SDXL, "tiny_xf": MODEL_TINY_XF, "sdxl_xf": MODEL_SDXL_XF}
 SCHEMES = {"pcpp": SCHEME_PCPP, "fullmap": SCHEME_FULLMAP, "sync": SCHEME_SYNC}
 
 
@@ -42,7 +45,8 @@ class pcpp_info(C.Structure):
                 ("bytes_counted_warmup", C.c_longlong * 3), ("last_step_ms", C.c_double),
                 ("device_bytes", C.c_longlong), ("n_kernels_per_step", C.c_int), ("graphs", C.c_int),
                 ("tc_kernels", C.c_int), ("step_flops", C.c_double), ("step_flops_rank_max", C.c_double),
-                ("arena_bytes_per_rank", C.c_longlong), ("arena_bytes_unplanned", C.c_longlong)]
+                ("arena_bytes_per_rank", C.c_longlong), ("arena_bytes_unplanned", C.c_longlong),
+                ("simt_fallbacks", C.c_int), ("backend", C.c_int), ("comm_lib", C.c_char * 192)]
 
     def as_dict(self):
         d = {}
@@ -50,6 +54,8 @@ class pcpp_info(C.Structure):
             v = getattr(self, name)
             if name in ("attn_h", "attn_r"):
                 v = list(v)[: self.n_attn]
+            elif name == "comm_lib":
+                v = v.decode()
             elif hasattr(v, "__len__"):
                 v = list(v)
             d[name] = v
@@ -64,7 +70,7 @@ SYMBOLS = ["pcpp_plan_schedule", "pcpp_profile", "pcpp_config_default", "pcpp_ge
            "pcpp_manifest_entry", "pcpp_plan", "pcpp_plan_info", "pcpp_set_cond", "pcpp_step",
            "pcpp_sample", "pcpp_reset", "pcpp_query", "pcpp_debug_comm_off", "pcpp_destroy", "pcpp_last_error",
            "pcpp_op_conv", "pcpp_op_attention", "pcpp_op_groupnorm", "pcpp_op_pack_rows",
-           "pcpp_op_cfg_ddim"]
+           "pcpp_op_cfg_ddim", "pcpp_peer_handle", "pcpp_peer_connect", "pcpp_set_context"]
 
 _lib = None
 
@@ -76,6 +82,14 @@ def lib():
         return _lib
     if not os.path.exists(LIB_PATH):
         raise RuntimeError(f"libpcpp.so not built ({LIB_PATH}); run python paper_2412_02962_b200/build.py")
+    if "PCPP_NCCL_LIB" not in os.environ:        # the NCCL torch ships (used by the NCCL backend only)
+        try:
+            import nvidia.nccl
+            cand = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["PCPP_NCCL_LIB"] = cand
+        except Exception:
+            pass
     L = C.CDLL(LIB_PATH)
     V, P, I, D, S = C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_size_t
     L.pcpp_config_default.argtypes = [C.POINTER(pcpp_config)]; L.pcpp_config_default.restype = None
@@ -86,6 +100,7 @@ def lib():
     L.pcpp_plan.argtypes = [I, I, I, I, D, I, C.POINTER(pcpp_config), C.POINTER(P)]; L.pcpp_plan.restype = I
     L.pcpp_plan_info.argtypes = [I, I, I, I, D, I, C.POINTER(pcpp_config), C.POINTER(pcpp_info)]; L.pcpp_plan_info.restype = I
     L.pcpp_set_cond.argtypes = [P, V]; L.pcpp_set_cond.restype = I
+    L.pcpp_set_context.argtypes = [P, V]; L.pcpp_set_context.restype = I
     L.pcpp_step.argtypes = [P, V, I]; L.pcpp_step.restype = I
     L.pcpp_sample.argtypes = [P, V, V, V]; L.pcpp_sample.restype = I
     L.pcpp_reset.argtypes = [P]; L.pcpp_reset.restype = I
@@ -102,6 +117,8 @@ def lib():
     L.pcpp_op_groupnorm.argtypes = [V, I, I, I, I, V, V, I, V, V, I, V]; L.pcpp_op_groupnorm.restype = I
     L.pcpp_op_pack_rows.argtypes = [V, C.c_longlong, I, I, V, V]; L.pcpp_op_pack_rows.restype = I
     L.pcpp_op_cfg_ddim.argtypes = [V, V, I, I, C.c_float, I, I, V]; L.pcpp_op_cfg_ddim.restype = I
+    L.pcpp_peer_handle.argtypes = [P, V]; L.pcpp_peer_handle.restype = I
+    L.pcpp_peer_connect.argtypes = [P, V]; L.pcpp_peer_connect.restype = I
     _lib = L
     return L
 
@@ -163,7 +180,7 @@ def make_config(model="sdxl", num_steps=50, guidance=5.0, precision="bf16", sche
     cfg.guidance_scale = guidance
     cfg.precision = BF16 if precision == "bf16" else FP32
     cfg.scheme = SCHEMES[scheme]
-    cfg.comm_backend = COMM_LOOPBACK if backend == "loopback" else COMM_NCCL
+    cfg.comm_backend = BACKENDS[backend]
     cfg.rank, cfg.world = rank, world
     cfg.kernels = KERNELS_AUTO if kernels == "auto" else KERNELS_SIMT
     cfg.use_graphs = 1 if graphs else 0
@@ -213,6 +230,11 @@ class Plan:
         c = np.ascontiguousarray(cond, dtype=np.float32)
         _chk(lib().pcpp_set_cond(self.h, c.ctypes.data), "pcpp_set_cond")
 
+    def pcpp_set_context(self, ctx: np.ndarray):
+        """_xf models: the cross-attention context [2, 77, ctx_dim] (b = 0 uncond, 1 cond)."""
+        c = np.ascontiguousarray(ctx, dtype=np.float32)
+        _chk(lib().pcpp_set_context(self.h, c.ctypes.data), "pcpp_set_context")
+
     def pcpp_step(self, latent, t: int):
         _chk(lib().pcpp_step(self.h, _ptr(latent), int(t)), "pcpp_step")
 
@@ -226,6 +248,17 @@ class Plan:
     def pcpp_sample_into(self, xT_ptr: int, cond_ptr: int, out_ptr: int):
         """Host pointers (e.g. pinned torch tensors)."""
         _chk(lib().pcpp_sample(self.h, xT_ptr, cond_ptr, out_ptr), "pcpp_sample")
+
+    def pcpp_peer_handle(self) -> bytes:
+        """PEER backend: this rank's 64-byte CUDA IPC handle of its arena."""
+        b = C.create_string_buffer(PEER_HANDLE_BYTES)
+        _chk(lib().pcpp_peer_handle(self.h, b), "pcpp_peer_handle")
+        return b.raw
+
+    def pcpp_peer_connect(self, handles: list[bytes]):
+        """PEER backend: open every rank's arena (handles in rank order)."""
+        buf = C.create_string_buffer(b"".join(handles), PEER_HANDLE_BYTES * len(handles))
+        _chk(lib().pcpp_peer_connect(self.h, buf), "pcpp_peer_connect")
 
     def pcpp_reset(self):
         _chk(lib().pcpp_reset(self.h), "pcpp_reset")

@@ -25,3 +25,13 @@ def cond(model: str):
     c = inputs.make_cond(M.arch(model)["temb"])
     c.setflags(write=False)
     return c
+
+
+@functools.lru_cache(maxsize=None)
+def context(model: str):
+    a = M.arch(model)
+    if not a["xf"]:
+        return None
+    c = inputs.make_context(M.CTX_LEN, a["ctx_dim"])
+    c.setflags(write=False)
+    return c

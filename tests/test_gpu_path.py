@@ -196,9 +196,11 @@ def test_ancestral_path_matches_oracle(cuda_ok, case):
     assert rel_l2(ref[0], other[0]) > 3 * rel_l2(xs[0], ref[0])
 
 
-def test_nccl_backend_single_rank_matches_loopback(cuda_ok):
-    """The NCCL backend (communicator init, graph capture with the comm stream, the final x_0
-    all-gather of pcpp_sample) at world = 1 reproduces the loopback backend bitwise."""
+def test_nccl_config_with_one_patch_runs_the_local_path(cuda_ok):
+    """A one-patch plan configured for NCCL has no neighbour: the library runs it on the local
+    (loopback) path -- no communicator, no exchange -- and says so in pcpp_query.backend; the sample is
+    bitwise the loopback plan's.  (The multi-process exchange itself is tests/test_gpu_peer.py; the
+    NCCL send/recv realisation needs >= 2 GPUs, which the in-round GPU box does not have.)"""
     import torch
     blob = weights("tiny", "bf16")
     cond = _data.cond("tiny")
@@ -215,6 +217,7 @@ def test_nccl_backend_single_rank_matches_loopback(cuda_ok):
         ch = torch.from_numpy(np.ascontiguousarray(cond, dtype=np.float32)).pin_memory()
         plan.pcpp_sample_into(xt.data_ptr(), ch.data_ptr(), x0.data_ptr())
         outs.append(x0.numpy().copy())
+        assert plan.pcpp_query()["backend"] == pcpp.COMM_LOOPBACK
         plan.close()
     assert np.array_equal(outs[0], outs[1])
 

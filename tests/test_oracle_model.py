@@ -105,3 +105,52 @@ def test_async_differs_from_sync_and_tracks_it():
     d = np.linalg.norm(a["x0"] - s["x0"]) / np.linalg.norm(s["x0"])
     assert 1e-6 < d < 0.5
     assert a["modes"] == ["sync", "async", "async", "async"]
+
+
+# ---- the SDXL transformer block variant ('_xf' models, reading D25/D26) ----------
+def test_xf_manifest_consistency_and_sdxl_size():
+    blob, xT, c = _inputs("tiny_xf", 32, 32)
+    P = M.Params("tiny_xf", blob)
+    M.unet(M.Ctx(1, 0.0, "sync"), P, "tiny_xf", [xT], M.timestep_embedding(P, "tiny_xf", 501, c), _data.context("tiny_xf"))
+    assert P.used == set(P.t), "every manifest tensor is used exactly by the forward"
+    # with SDXL's transformer blocks the SDXL-shaped stack has SDXL's UNet size (2.567 B parameters)
+    n = sum(int(np.prod(s)) for _, s, _ in M.manifest("sdxl_xf"))
+    assert 2.55e9 < n < 2.58e9, n
+
+
+def test_xf_requires_context():
+    blob, xT, c = _inputs("tiny_xf", 32, 32)
+    P = M.Params("tiny_xf", blob)
+    with pytest.raises(ValueError):
+        M.unet(M.Ctx(1, 0.0, "sync"), P, "tiny_xf", [xT], M.timestep_embedding(P, "tiny_xf", 501, c))
+
+
+@pytest.mark.parametrize("tau", [981, 1])
+def test_P1_xf_one_patch_equals_unpartitioned_network(tau):
+    blob, xT, c = _inputs("tiny_xf", 32, 32)
+    ctxt = _data.context("tiny_xf")
+    P = M.Params("tiny_xf", blob)
+    emb = M.timestep_embedding(P, "tiny_xf", tau, c)
+    e = M.unet(M.Ctx(1, 0.3, "sync"), P, "tiny_xf", [xT.astype(np.float64)], emb, ctxt)[0]
+    ref = torch_ref.eps("tiny_xf", blob, xT, tau, c, ctxt)
+    np.testing.assert_allclose(e, ref, atol=1e-11 * max(1.0, np.abs(ref).max()))
+
+
+@pytest.mark.parametrize("n,p", [(2, 0.25), (4, 0.5)])
+def test_P2_P6_xf(n, p):
+    blob, xT, c = _inputs("tiny_xf", 32, 32)
+    ctxt = _data.context("tiny_xf")
+    # P2: all-synchronous n-patch sampling == single device
+    a = pcpp.sample(pcpp.Config(model="tiny_xf", n=1, p=0.0, warmup=3, steps=3), blob, xT, c, context=ctxt)
+    b = pcpp.sample(pcpp.Config(model="tiny_xf", n=n, p=p, warmup=3, steps=3), blob, xT, c, context=ctxt)
+    for xa, xb in zip(a["xs"], b["xs"]):
+        np.testing.assert_allclose(xb, xa, atol=1e-12 * np.abs(xa).max())
+    # P6: fresh then async on the same input reproduces fresh (the new layers are patch-local)
+    e1, e2 = pcpp.forward_pair(pcpp.Config(model="tiny_xf", n=n, p=p), blob, xT, 501, c, "fresh", "async", ctxt)
+    for u, v in zip(e1, e2):
+        np.testing.assert_allclose(v, u, atol=1e-11 * max(1.0, np.abs(u).max()))
+    # P3: n = 2, p = 1, fresh == single device (cross-attention and FF change nothing in the argument)
+    if n == 2:
+        ef, _ = pcpp.forward_pair(pcpp.Config(model="tiny_xf", n=2, p=1.0), blob, xT, 751, c, "fresh", "fresh", ctxt)
+        ref = torch_ref.eps("tiny_xf", blob, xT, 751, c, ctxt)
+        np.testing.assert_allclose(np.concatenate(ef, axis=1), ref, atol=1e-11 * max(1.0, np.abs(ref).max()))

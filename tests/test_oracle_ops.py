@@ -174,3 +174,60 @@ def test_attention_band_assembly_matches_masked_global_attention(n, p):
                 s = np.exp(s - s.max(1, keepdims=True)); s /= s.sum(1, keepdims=True)
                 out[:, sl] = s @ V[b].reshape(-1, C)[:, sl]
             np.testing.assert_allclose(y[i][b].reshape(-1, C), out @ wo.T + bo, atol=1e-12)
+
+
+# ---- transformer-block ops of the '_xf' models (reading D25) --------------------------------------
+def test_layer_norm_equals_torch_and_closed_forms():
+    import torch
+    import torch.nn.functional as F
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((2, 3, 5, 128)) * 3 + 1
+    g, b = rng.standard_normal(128), rng.standard_normal(128)
+    y = M.layer_norm([x], g, b)[0]
+    ref = F.layer_norm(torch.from_numpy(x), (128,), torch.from_numpy(g), torch.from_numpy(b), eps=1e-5).numpy()
+    np.testing.assert_allclose(y, ref, atol=1e-12)
+    # gamma = 1, beta = 0: zero mean and (nearly) unit variance per token; a constant token -> beta
+    z = M.layer_norm([x], np.ones(128), np.zeros(128))[0]
+    np.testing.assert_allclose(z.mean(axis=-1), 0, atol=1e-12)
+    np.testing.assert_allclose(z.var(axis=-1), 1 / (1 + 1e-5 / x.var(axis=-1)), rtol=1e-10)
+    c = M.layer_norm([np.full((1, 1, 1, 128), 7.0)], g, b)[0]
+    np.testing.assert_allclose(c[0, 0, 0], b, atol=1e-12)
+
+
+def test_cross_attention_equals_sdpa_and_closed_forms():
+    import torch
+    import torch.nn.functional as F
+    rng = np.random.default_rng(6)
+    C, D = 128, 32
+    x = rng.standard_normal((2, 3, 4, C))
+    ctx = rng.standard_normal((2, 77, D))
+    wq, wk, wv, wo = (rng.standard_normal(s) / 8 for s in ((C, C), (C, D), (C, D), (C, C)))
+    bo = rng.standard_normal(C)
+    y = M.cross_attention([x], ctx, wq, wk, wv, wo, bo)[0]
+    t = lambda a: torch.from_numpy(a)
+    q = (t(x).reshape(2, 12, C) @ t(wq).T).reshape(2, 12, 2, 64).transpose(1, 2)
+    k = (t(ctx) @ t(wk).T).reshape(2, 77, 2, 64).transpose(1, 2)
+    v = (t(ctx) @ t(wv).T).reshape(2, 77, 2, 64).transpose(1, 2)
+    o = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(2, 12, C) @ t(wo).T + t(bo)
+    np.testing.assert_allclose(y, o.reshape(2, 3, 4, C).numpy(), atol=1e-12)
+    # identical context tokens -> every query sees mean(V) = that token's value
+    same = np.repeat(ctx[:, :1], 77, axis=1)
+    y2 = M.cross_attention([x], same, wq, wk, wv, np.eye(C), np.zeros(C))[0]
+    np.testing.assert_allclose(y2, np.broadcast_to((same[:, 0] @ wv.T)[:, None, None, :], y2.shape), atol=1e-12)
+
+
+def test_gelu_geglu_closed_forms():
+    import torch
+    import torch.nn.functional as F
+    x = np.linspace(-6, 6, 121)
+    np.testing.assert_allclose(M.gelu(x), F.gelu(torch.from_numpy(x)).numpy(), atol=1e-14)
+    assert M.gelu(np.array([0.0]))[0] == 0.0
+    np.testing.assert_allclose(M.gelu(np.array([1.0]))[0], 0.8413447460685429, atol=1e-15)  # Phi(1)
+    # GEGLU: value half [I; 0], gate half [0; big I] -> FF(x) ~ x * gelu(big * x) ~ relu-gated identity
+    C = 4
+    w1 = np.zeros((8 * C, C)); w1[:C] = np.eye(C); w1[4 * C:5 * C] = 1e3 * np.eye(C)
+    w2 = np.zeros((C, 4 * C)); w2[:, :C] = np.eye(C)
+    x = np.array([[[[1.5, -2.0, 0.25, -0.125]]]])
+    y = M.geglu_ff([x], w1, np.zeros(8 * C), w2, np.zeros(C))[0]
+    np.testing.assert_allclose(y, x * M.gelu(1e3 * x), atol=1e-12)
+    np.testing.assert_allclose(y, np.where(x > 0, 1e3 * x * x, 0.0), rtol=1e-12, atol=1e-12)
