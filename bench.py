@@ -43,12 +43,15 @@ def parse():
     ap.add_argument("--backend", default="peer", choices=["peer", "nccl"],
                     help="N > 1 exchange transport: one-sided peer stores (default) or NCCL send/recv")
     ap.add_argument("--e2e-samples", type=int, default=5)
+    ap.add_argument("--cfg-split", action="store_true",
+                    help="the paper's CFG device split (P:24): N GPUs = 2 branch groups x N/2 patches")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-comm-off", action="store_true", help="N > 1: skip the COMM_OFF re-timing")
     ap.add_argument("--no-loopback", action="store_true", help="skip the n = 2/4/8 loopback projections (N = 1)")
     ap.add_argument("--no-large", action="store_true", help="skip the 2048^2 / 3840^2 lines (N = 1)")
+    ap.add_argument("--no-xf", action="store_true", help="skip the SDXL-transformer-block (sdxl_xf) line (N = 1)")
     ap.add_argument("--kernels", default="auto", choices=["auto", "simt"])
     return ap.parse_args()
 
@@ -243,13 +246,15 @@ def time_steps(plan, lat, first, count, torch):
     return e0.elapsed_time(e1) / count
 
 
-def loopback_line(pcpp, torch, np, inputs, res, nv, pv, scheme, S, cond, kernels, blob, comm_off=True):
-    """All n virtual ranks of an n-patch plan back to back on this GPU (LOOPBACK: exchanges are device
-    copies of exactly the bytes the transports move); ms/step of all ranks / n = the mean per-rank step
-    -- a projection of one rank on its own GPU, not a multi-GPU measurement."""
+def loopback_line(pcpp, torch, np, inputs, res, nv, pv, scheme, S, cond, kernels, blob, comm_off=True, split=False):
+    """All virtual ranks of an n-patch plan back to back on this GPU (LOOPBACK: exchanges are device
+    copies of exactly the bytes the transports move); ms/step of all ranks / ranks = the mean per-rank
+    step -- a projection of one rank on its own GPU, not a multi-GPU measurement.  split: the CFG
+    device split, 2 x n ranks of batch 1."""
     wv = 4 if nv > 1 else 0
+    ranks = 2 * nv if split else nv
     cfg = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme=scheme, backend="loopback",
-                           kernels=kernels)
+                           kernels=kernels, cfg_split=split)
     pl = pcpp.Plan(res, res, 4, nv, pv, wv, cfg, blob)
     pl.pcpp_set_cond(cond)
     lat = torch.from_numpy(np.ascontiguousarray(inputs.make_latent(res, res))).cuda()
@@ -267,10 +272,11 @@ def loopback_line(pcpp, torch, np, inputs, res, nv, pv, scheme, S, cond, kernels
         pl.pcpp_debug_comm_off(False)
     info = pl.pcpp_query()
     pl.close()
-    return {"scheme": scheme, "n": nv, "p": pv, "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / nv, 4),
+    return {"scheme": scheme + ("+cfg_split" if split else ""), "n_patches": nv, "gpus": ranks, "p": pv,
+            "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / ranks, 4),
             "ms_per_step_all_ranks_comm_off": t_off, "step_flops_rank_max": info["step_flops_rank_max"],
-            "bytes_exchanged_per_step": sum(info["bytes_counted_async"]),
-            "bytes_by_class": dict(zip(("attn", "conv", "gn"), info["bytes_counted_async"]))}
+            "bytes_exchanged_per_step": sum(info["bytes_counted_async"]) + info["bytes_eps"],
+            "bytes_by_class": dict(zip(("attn", "conv", "gn", "eps"), info["bytes_counted_async"] + [info["bytes_eps"]]))}
 
 
 def main():
@@ -299,11 +305,15 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = N
+    split = args.cfg_split and N > 1
+    if split and N % 2:
+        raise SystemExit("--cfg-split needs an even number of GPUs")
+    n = N // 2 if split else N          # patches (per branch group with the split)
     p = P_BY_N.get(n, 0.8) if args.p is None else args.p
     w = 4 if n > 1 else 0
     H = W = args.res
     h = H // n
+    patch_id = rank % n
     pre = max(args.warmup, w)
     S = max(50, pre + args.steps)
 
@@ -320,7 +330,7 @@ def main():
             dist.broadcast(idt, 0)
             nccl_id = bytes(idt.cpu().numpy().tobytes())
         cfg = pcpp.make_config(model="sdxl", num_steps=S, precision="bf16", scheme=args.scheme, backend=backend,
-                               rank=rank, world=max(world, 1), nccl_id=nccl_id, kernels=args.kernels)
+                               rank=rank, world=max(world, 1), nccl_id=nccl_id, kernels=args.kernels, cfg_split=split)
         pl = pcpp.Plan(H, W, 4, n, p, w, cfg, blob)
         if backend == "peer":
             handles = [None] * world
@@ -348,7 +358,7 @@ def main():
         plan = make_plan(backend)
     _progress(f"plan built ({backend}; weights uploaded, GEMMs autotuned, graphs pending)")
     plan.pcpp_set_cond(cond)
-    patch = xT[rank * h:(rank + 1) * h] if world > 1 else xT
+    patch = xT[patch_id * h:(patch_id + 1) * h] if world > 1 else xT
     lat = torch.from_numpy(np.ascontiguousarray(patch)).cuda()
 
     def barrier():
@@ -483,6 +493,12 @@ def main():
                 r = loopback_line(pcpp, torch, np, inputs, H, nv, P_BY_N[nv], sch, S, cond, args.kernels, blob2)
                 r["projected_speedup_vs_n1"] = round(ms / r["ms_per_rank"], 2)
                 loop[f"n{nv}" + ("" if sch == "pcpp" else "_fullmap")] = r
+            for gpus in (2, 4, 8):          # the paper's deployment: CFG split, gpus / 2 patches per branch
+                nv = gpus // 2
+                r = loopback_line(pcpp, torch, np, inputs, H, nv, P_BY_N.get(nv, 0.0), "pcpp", S, cond, args.kernels,
+                                  blob2, comm_off=False, split=True)
+                r["projected_speedup_vs_n1"] = round(ms / r["ms_per_rank"], 2)
+                loop[f"gpus{gpus}_cfg_split"] = r
             loop["note"] = ("loopback: the n virtual ranks run sequentially on one GPU, exchanges are device copies; "
                             "ms_per_rank = all-rank time / n (a projection of one rank on its own GPU, not measured); "
                             "n8_fullmap = the DistriFusion-style full-map exchange (P:86) on the same kernels")
@@ -512,6 +528,35 @@ def main():
                              "projections (ms_per_rank = all-rank time / n)")
         del blob2
 
+    # the SDXL-faithful stack: every attention layer a full transformer block (LN,
+    # self-attn, LN, cross-attn to 77 tokens, LN, GEGLU FF; 2.57 B parameters), N = 1 and an n = 8 projection
+    xf = None
+    if rank == 0 and world == 1 and args.scheme == "pcpp" and args.res == 128 and not args.no_xf:
+        xf = {}
+        blob3 = inputs.make_weight_blob(inputs.init_specs(pcpp.manifest("sdxl_xf")))
+        ctxt = inputs.make_context(77, 2048)
+        for nv in (1, 8):
+            wv = 4 if nv > 1 else 0
+            cfg3 = pcpp.make_config(model="sdxl_xf", num_steps=S, precision="bf16", backend="loopback", kernels=args.kernels)
+            pl = pcpp.Plan(H, W, 4, nv, P_BY_N[nv], wv, cfg3, blob3)
+            pl.pcpp_set_cond(cond)
+            pl.pcpp_set_context(ctxt)
+            lat3 = torch.from_numpy(np.ascontiguousarray(xT)).cuda()
+            for k in range(wv + 2):
+                pl.pcpp_step(lat3, k)
+            t = time_steps(pl, lat3, wv + 2, 5, torch)
+            inf3 = pl.pcpp_query()
+            pl.close()
+            xf[f"n{nv}"] = {"ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / nv, 4),
+                            "step_flops_rank_max": inf3["step_flops_rank_max"],
+                            "achieved_tflops_rank": round(inf3["step_flops_rank_max"] / (t / nv * 1e-3) / 1e12, 1),
+                            "simt_fallbacks": inf3["simt_fallbacks"]}
+        xf["projected_speedup_n8"] = round(xf["n1"]["ms_per_rank"] / xf["n8"]["ms_per_rank"], 2)
+        xf["note"] = ("sdxl_xf = SDXL's transformer blocks (2.57 B parameters, SDXL's UNet size); n = 8 is a loopback "
+                      "projection (all-rank time / 8)")
+        del blob3
+        _progress("sdxl_xf lines done")
+
     if rank == 0:
         cls = ("attn", "conv", "gn")
         out = {
@@ -519,15 +564,17 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: seeded N(0,1) latent and cond, random-init SDXL-shaped weights (no checkpoint offline)",
-            "config": {"workload": f"sdxl-{H * 8} ({H}x{W}x4 latent, 50-step DDIM schedule, CFG s=5 as batch 2)",
+            "config": {"workload": f"sdxl-{H * 8} ({H}x{W}x4 latent, 50-step DDIM schedule, CFG s=5 "
+                                   + ("split over 2 GPU groups)" if split else "as batch 2)"),
                        "model": "SDXL-shaped UNet stack (70 self-attn, 40 conv3x3, 46 GN; SURVEY App. A)",
-                       "global_batch": 2, "seq_len": H * W, "parallelism": f"pcpp-patch{n}",
+                       "global_batch": 2, "seq_len": H * W,
+                       "parallelism": f"pcpp-patch{n}" + ("-cfgsplit2" if split else ""), "cfg_split": split,
                        "n_patches": n, "cond_fraction": p, "warmup_steps": w, "num_steps": S,
                        "scheme": args.scheme, "step_flops_per_rank": info["step_flops_rank_max"],
                        "backend": ["nccl", "loopback", "peer"][info["backend"]], "backend_note": backend_note,
                        "simt_fallbacks_per_step": info["simt_fallbacks"],
                        "l2": "per-step working set (1.57 GB bf16 weights + activations) >> 126 MB L2; no flush"},
-            "bytes_exchanged_per_step": {"async": dict(zip(cls, info["bytes_counted_async"])),
+            "bytes_exchanged_per_step": {"async": dict(zip(cls, info["bytes_counted_async"])), "eps_cfg_split": info["bytes_eps"],
                                          "warmup": dict(zip(cls, info["bytes_counted_warmup"])),
                                          "fullmap_async": dict(zip(cls, info["bytes_fullmap"]))},
             "achieved_tflops_step": round(info["step_flops_rank_max"] / (ms * 1e-3) / 1e12, 1),
@@ -536,7 +583,8 @@ def main():
             "e2e": e2e, "roofline": roof, "roofline_attention": roof_attn, "roofline_groupnorm": roof_gn,
             "cpu_baseline": cpu,
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in prof.items()},
-            "pcpp_loopback_1gpu": loop, "sw_sweep_1024_n8": sweep, "large_resolutions": large, "comm_off": comm_off,
+            "pcpp_loopback_1gpu": loop, "sw_sweep_1024_n8": sweep, "large_resolutions": large, "sdxl_xf_1024": xf,
+            "comm_off": comm_off,
             "context": "paper: 2.36-8.02x speed-up on 4-8 A100-40GB, SDXL fp16 (P:5); not comparable hardware",
             "bench_wall_s": round(time.time() - T_START, 1),
         }

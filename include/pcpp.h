@@ -65,7 +65,7 @@ enum { PCPP_KERNELS_AUTO = 0, PCPP_KERNELS_SIMT = 1 };        /* bf16: tcgen05 k
 typedef struct pcpp_plan_s* pcpp_plan_t;                     /* opaque; owned by libpcpp */
 
 typedef struct {
-  int rank, world;            /* NCCL: this process's rank, world == n_patches.  Rank r owns latent
+  int rank, world;            /* NCCL / PEER: this process's rank, world == n_patches (x 2 with cfg_split).  Rank r owns latent
                                  rows [r*H/n, (r+1)*H/n).  LOOPBACK: ignored (all n virtual ranks
                                  run in this process on one GPU). */
   int num_steps;              /* S (DDIM steps), >= 1; 50 in the paper */
@@ -89,6 +89,13 @@ typedef struct {
                                  Elementwise and patch-local: no exchange. */
   unsigned long long noise_seed; /* ANCESTRAL: key of the counter-based noise z (Philox4x64-10 on
                                  (global latent token, step); independent of n and of the rank) */
+  int cfg_split;              /* 1: the CFG device split of DistriFusion / the paper (§2.2; P:134, P:155:
+                                 "4 devices = 2 patches"): world = 2 * n_patches ranks; rank r runs CFG branch
+                                 r / n (0 uncond, 1 cond) as batch 1 on patch r % n, exchanges bands / halos /
+                                 GN sums within its branch group, and swaps eps with its partner (same patch,
+                                 other branch) every step before CFG + DDIM.  PEER / LOOPBACK backends, non-_XF
+                                 models (PCPP_ERR_UNSUPPORTED otherwise).  0 (default): CFG as batch 2 on every
+                                 rank (reading D11). */
 } pcpp_config;
 
 #define PCPP_SCHED_DDIM 0
@@ -125,6 +132,7 @@ typedef struct {
                                            the SIMT kernel (unsupported shape); 0 on every SDXL/tiny shape */
   int backend;                          /* effective PCPP_COMM_* (n == 1 always runs LOOPBACK) */
   char comm_lib[192];                   /* NCCL backend: path of the libnccl that was loaded ("" otherwise) */
+  long long bytes_eps;                  /* cfg_split: eps bytes swapped between branch partners per step (all ranks) */
 } pcpp_info;
 
 /* ---- setup ------------------------------------------------------------------------------- */

@@ -36,6 +36,10 @@ struct GemmArgs {
   // gn_part [slots][B=2][G=32][2] fp64 and *gn_slots (host) receives the slot count, 0 if the
   // launch did not produce them (the consumer then runs the standalone stats kernel)
   double* gn_part = nullptr; int* gn_slots = nullptr;
+  // GEGLU epilogue (the _XF feed-forward, reading D25): D has N columns in 64-column blocks
+  // [value 64 | gate 64] (the builder interleaves W_ff1's rows); out gets N / 2 columns
+  // out[:, 64 k + j] = (D[:, 128 k + j] + bias) * gelu(D[:, 128 k + 64 + j] + bias)
+  int geglu = 0;
 };
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 
@@ -86,7 +90,8 @@ struct GnApplyArgs {
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s);
 
 // SDXL transformer block (kernels/xformer.cu; reading D25): LayerNorm of every token over its C
-// channels (false if C is unsupported); GEGLU gate out = u[:, :4C] * gelu(u[:, 4C:]); the context
+// channels (false if C is unsupported); GEGLU gate out[:, 64k + j] = u[:, 128k + j] * gelu(u[:, 128k + 64 + j])
+// (u in the blocked [value 64 | gate 64] column order of the interleaved W_ff1); the context
 // [B][L][D] fp32 laid out as the rows of a [rows][B][W][D] key source (keys >= L zero)
 bool launch_layernorm(const ActView& x, const ActView& y, const float* gamma, const float* beta, cudaStream_t s);
 void launch_geglu(const ActView& u, const ActView& out, cudaStream_t s);

@@ -8,22 +8,21 @@
 namespace pcpp {
 
 // ---- latent [h][W][4] fp32 -> xin [h][2][W][4] fp32 (rows 0..h-1; halos untouched) ------------
-__global__ void prep_latent_kernel(const float4* __restrict__ lat, float4* __restrict__ xin, int h, int W) {
+__global__ void prep_latent_kernel(const float4* __restrict__ lat, float4* __restrict__ xin, int h, int W, int B) {
   pdl_trigger();
   pdl_wait();
   const long long n = (long long)h * W;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / W, w = i % W;
     const float4 v = lat[i];
-    xin[(r * 2 + 0) * W + w] = v;
-    xin[(r * 2 + 1) * W + w] = v;
+    for (int b = 0; b < B; ++b) xin[(r * B + b) * W + w] = v;     // every CFG branch held by this rank
   }
 }
 void launch_prep_latent(const float* latent, const ActView& xin, cudaStream_t s) {
   const long long n = (long long)xin.rows * xin.W;
   int blocks = (int)((n + 255) / 256); if (blocks > 1184) blocks = 1184;
   launch_pdl(prep_latent_kernel, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const float4*>(latent),
-                                             reinterpret_cast<float4*>(xin.base), xin.rows, xin.W);
+                                             reinterpret_cast<float4*>(xin.base), xin.rows, xin.W, xin.B);
 }
 
 // ---- nearest x2 upsample (16-byte vectors) ------------------------------------------------------

@@ -26,6 +26,8 @@ struct TcGemmParams {
   int nk0, nkc, taps, pad, stride;
   int rows_out, w_out, B;
   int Wbox, Bbox, Rbox, nWt, m_tiles;
+  int rowtile;                // tiles of whole rows (all batch entries) when W < 128
+  int geglu;                  // GEGLU epilogue (GemmArgs::geglu): out col 64k + j = v * gelu(g), N/2 cols
   int N, n_split;
   unsigned a_bytes;
   const float* bias; const float* temb; int temb_ld;
@@ -157,6 +159,39 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
   const long long orow = (((long long)r * ov.B + b) * ov.W + w) * ov.C + ncol0;
   const long long rrow = res_row(p, r, b, w, n0);
   uint4 rcur[4] = {rres0[0], rres0[1], rres0[2], rres0[3]}, rnext[4];
+  if (!ST && p.geglu) {
+    // blocks of 128 accumulator columns = [value 64 | gate 64] -> 64 output columns (bf16)
+    const long long grow = (((long long)r * p.out.B + b) * p.out.W + w) * p.out.C + n0 / 2;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 128) {
+#pragma unroll 1
+      for (int hh = 0; hh < 64; hh += 32) {
+        uint32_t va[32], vg[32];
+        sm100::tmem_ld32(tacc + c + hh, va);
+        sm100::tmem_ld32(tacc + c + 64 + hh, vg);
+        sm100::tmem_wait_ld();
+        if (!valid) continue;
+        float f[32];
+        const float4* ba = reinterpret_cast<const float4*>(p.bias + n0 + c + hh);
+        const float4* bg = reinterpret_cast<const float4*>(p.bias + n0 + c + 64 + hh);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 x = __ldg(ba + i), y = __ldg(bg + i);
+          const float xa[4] = {x.x, x.y, x.z, x.w}, yg[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float a = __uint_as_float(va[4 * i + e]) + xa[e];
+            const float g = __uint_as_float(vg[4 * i + e]) + yg[e];
+            f[4 * i + e] = a * (0.5f * g * (1.f + erff(g * 0.70710678118654752f)));
+          }
+        }
+        bf16* po = reinterpret_cast<bf16*>(p.out.base) + grow + c / 2 + hh;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) store8(po + 8 * j, f + 8 * j);
+      }
+    }
+    return;
+  }
   if (p.splits > 1) {
     // split-K: raw fp32 partial tile -> workspace; gemm_splitk_finish applies the epilogue
     const long long T = ((long long)r * p.B + b) * p.w_out + w;
@@ -267,7 +302,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
     const int rest = u / p.m_tiles;
     n0 = (rest % n_tiles) * BN;
     z = rest / n_tiles;
-    if (p.Bbox == 2) { r0 = mt * p.Rbox; b0 = 0; w0 = 0; }
+    if (p.rowtile) { r0 = mt * p.Rbox; b0 = 0; w0 = 0; }
     else { const int wt = mt % p.nWt; const int tb = mt / p.nWt; b0 = tb % p.B; r0 = tb / p.B; w0 = wt * p.Wbox; }
   };
 
@@ -423,6 +458,7 @@ static int pick_bn(const GemmArgs& g) {
   const int cands[4] = {256, 160, 128, 64};
   for (int bn : cands) {
     if (g.N % bn) continue;
+    if (g.geglu && bn % 128) continue;
     if (g.n_split < g.N && g.n_split % bn) continue;
     return bn;
   }
@@ -439,7 +475,9 @@ bool gemm_tc_supported(const GemmArgs& g) {
   if (g.res.base && g.res.dtype != DT_BF16) return false;
   if (g.out2.base && g.out2.dtype != g.out.dtype) return false;
   if (!pick_bn(g)) return false;
-  if (g.B != 2 && g.w_out < 128) return false;
+  if (g.geglu && (g.N % 128 || g.res.base || g.out2.base || g.out.dtype != DT_BF16 || !g.bias || g.temb || g.out.C * 2 != g.N))
+    return false;
+  if (g.w_out < 128 && 128 % (g.B * g.w_out) != 0 && g.B != 2) return false;
   return true;
 }
 
@@ -514,7 +552,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
     n0 = (rest % n_tiles) * BN;
     z = rest / n_tiles;
     const int mt = 2 * mp + (int)rank;
-    if (p.Bbox == 2) { r0 = mt * p.Rbox; b0 = 0; w0 = 0; }
+    if (p.rowtile) { r0 = mt * p.Rbox; b0 = 0; w0 = 0; }
     else { const int wt = mt % p.nWt; const int tb = mt / p.nWt; b0 = tb % p.B; r0 = tb / p.B; w0 = wt * p.Wbox; }
   };
 
@@ -693,7 +731,7 @@ void gemm_tc_init() {
 
 // ---- configuration choice: per-shape autotune cache (filled at plan time), else a heuristic ----
 struct GemmKey {
-  int rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt, st;
+  int rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt, st;   // st: 2 = GEGLU epilogue
   bool operator<(const GemmKey& o) const {
     const int a[12] = {rows_out, w_out, B, N, cin, c0, taps, stride, split_out, res, odt, st};
     const int b[12] = {o.rows_out, o.w_out, o.B, o.N, o.cin, o.c0, o.taps, o.stride, o.split_out, o.res, o.odt, o.st};
@@ -708,7 +746,7 @@ static bool gn_fusable(const GemmArgs& g) {
 }
 static GemmKey key_of(const GemmArgs& g) {
   return GemmKey{g.rows_out, g.w_out, g.B, g.N, g.cin, g.c0, g.taps, g.stride, g.n_split < g.N ? g.n_split : 0,
-                 g.res.base ? 1 : 0, g.out.dtype, gn_fusable(g) ? 1 : 0};
+                 g.res.base ? 1 : 0, g.out.dtype, g.geglu ? 2 : (gn_fusable(g) ? 1 : 0)};
 }
 struct GemmChoice { int bn, splits, pair; };
 static std::map<GemmKey, GemmChoice>& tune_cache() { static std::map<GemmKey, GemmChoice> m; return m; }
@@ -716,6 +754,7 @@ static std::mutex& tune_mu() { static std::mutex m; return m; }
 
 static bool bn_ok(const GemmArgs& g, int bn) {
   if (g.N % bn) return false;
+  if (g.geglu && bn % 128) return false;
   if (g.n_split < g.N && g.n_split % bn) return false;
   return true;
 }
@@ -724,11 +763,13 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   TcGemmParams p;
   memset(&p, 0, sizeof p);
   // tile geometry: 128 output tokens = Wbox x Bbox x Rbox in (w, b, r) layout order
+  // tile = 128 output tokens: a 128-wide row segment, or whole rows of every batch entry (W < 128)
+  p.rowtile = g.w_out < 128 && 128 % (g.B * g.w_out) == 0;
   if (g.w_out >= 128) { p.Wbox = 128; p.Bbox = 1; p.Rbox = 1; }
-  else if (g.B == 2 && 128 % (2 * g.w_out) == 0) { p.Wbox = g.w_out; p.Bbox = 2; p.Rbox = 128 / (2 * g.w_out); }
+  else if (p.rowtile) { p.Wbox = g.w_out; p.Bbox = g.B; p.Rbox = 128 / (g.B * g.w_out); }
   else { p.Wbox = g.w_out; p.Bbox = 1; p.Rbox = 1; }
   p.nWt = (g.w_out + p.Wbox - 1) / p.Wbox;
-  if (p.Bbox == 2) p.m_tiles = (g.rows_out + p.Rbox - 1) / p.Rbox;
+  if (p.rowtile) p.m_tiles = (g.rows_out + p.Rbox - 1) / p.Rbox;
   else p.m_tiles = g.rows_out * g.B * p.nWt;
   p.taps = g.taps; p.pad = g.taps == 9 ? 1 : 0; p.stride = g.stride;
   p.nkc = g.cin / 64; p.nk0 = g.c0 / 64;
@@ -737,6 +778,8 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   p.a_bytes = 128u * p.Wbox * p.Bbox * p.Rbox;
   p.bias = g.bias; p.temb = g.temb; p.temb_ld = g.temb_ld;
   p.res = g.res; p.out = g.out; p.out2 = g.out2;
+  p.geglu = g.geglu;
+  if (g.geglu) want_splits = 1;
   if (!encode_act(&p.ma0, g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_act(&p.ma1, g.a1.base ? g.a1 : g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN)) return false;
@@ -782,7 +825,7 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
 static GemmChoice heuristic(const GemmArgs& g) {
   GemmChoice c{pick_bn(g), 1, 0};
   const int m_tiles = g.w_out >= 128 ? g.rows_out * g.B * ((g.w_out + 127) / 128)
-                      : (g.B == 2 && 128 % (2 * g.w_out) == 0) ? (g.rows_out + 128 / (2 * g.w_out) - 1) / (128 / (2 * g.w_out))
+                      : (128 % (g.B * g.w_out) == 0) ? (g.rows_out + 128 / (g.B * g.w_out) - 1) / (128 / (g.B * g.w_out))
                       : g.rows_out * g.B;
   const long long tiles = (long long)m_tiles * (g.N / c.bn);
   const int nsteps = g.taps * (g.cin / 64);
@@ -862,7 +905,7 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
     if (!bn_ok(g, bn)) continue;
     if (pair && bn == 64) continue;
     for (int S = 1; S <= 6; ++S) {
-      if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems || gn_fusable(g))) break;
+      if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems || gn_fusable(g) || g.geglu)) break;
       if (!launch_gemm_tc_cfg(g, s, bn, S, pair)) continue;      // warm
       cudaEventRecord(e0, s);
       for (int r = 0; r < 3; ++r) launch_gemm_tc_cfg(g, s, bn, S, pair);

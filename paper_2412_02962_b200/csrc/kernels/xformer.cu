@@ -79,8 +79,10 @@ bool launch_layernorm(const ActView& x, const ActView& y, const float* g, const 
   return true;
 }
 
-// GEGLU gate: u = [value (4C) | gate (4C)] per token -> out = value * gelu(gate), exact GELU
-// (x Phi(x) with erff; SDXL's GEGLU uses the exact form, reading D25).
+// GEGLU gate: u per token in 64-column blocks [value 64 | gate 64] (the builder interleaves the rows of
+// W_ff1 = [W_value; W_gate] so that the fused GEMM epilogue sees a value column and its gate in one
+// tile) -> out = value * gelu(gate), exact GELU (x Phi(x) with erff; reading D25).  The unfused path
+// (fp32 parity mode / SIMT GEMM).
 template <typename T>
 __global__ void __launch_bounds__(256) geglu_kernel(const T* __restrict__ u, T* __restrict__ out, long long ntok, int C4) {
   pdl_trigger();
@@ -90,9 +92,10 @@ __global__ void __launch_bounds__(256) geglu_kernel(const T* __restrict__ u, T* 
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long t = i / nv;
     const int c = (int)(i - t * nv) * 8;
+    const int uc = (c >> 6) * 128 + (c & 63);     // value column of output column c in the blocked order
     float a[8], g[8];
-    load8(u + t * 2 * C4 + c, a);
-    load8(u + t * 2 * C4 + C4 + c, g);
+    load8(u + t * 2 * C4 + uc, a);
+    load8(u + t * 2 * C4 + uc + 64, g);
 #pragma unroll
     for (int e = 0; e < 8; ++e) a[e] *= 0.5f * g[e] * (1.f + erff(g[e] * 0.70710678118654752f));
     store8(out + t * C4 + c, a);

@@ -46,13 +46,22 @@ pcpp_status validate(int H, int W, int C, int n, double p, int w, const pcpp_con
   }
   if (cfg->precision != PCPP_FP32 && cfg->precision != PCPP_BF16) { set_error("bad precision"); return PCPP_ERR_INVALID; }
   if (cfg->scheme < 0 || cfg->scheme > 2) { set_error("bad scheme"); return PCPP_ERR_INVALID; }
+  if (cfg->cfg_split != 0 && cfg->cfg_split != 1) { set_error("cfg_split must be 0 or 1"); return PCPP_ERR_INVALID; }
+  if (cfg->cfg_split && (cfg->model == PCPP_MODEL_TINY_XF || cfg->model == PCPP_MODEL_SDXL_XF)) {
+    set_error("cfg_split with the _XF models is not supported"); return PCPP_ERR_UNSUPPORTED;
+  }
+  if (cfg->cfg_split && cfg->comm_backend == PCPP_COMM_NCCL) {
+    set_error("cfg_split needs the PEER or LOOPBACK backend (NCCL would need per-branch communicators)"); return PCPP_ERR_UNSUPPORTED;
+  }
   if (cfg->comm_backend == PCPP_COMM_NCCL) {
     if (cfg->world != n) { set_error("world (%d) must equal n_patches (%d)", cfg->world, n); return PCPP_ERR_INVALID; }
     if (cfg->rank < 0 || cfg->rank >= n) { set_error("rank out of range"); return PCPP_ERR_INVALID; }
     if (n > 1 && !cfg->nccl_id) { set_error("nccl_id required for the NCCL backend"); return PCPP_ERR_INVALID; }
   } else if (cfg->comm_backend == PCPP_COMM_PEER) {
-    if (cfg->world != n) { set_error("world (%d) must equal n_patches (%d)", cfg->world, n); return PCPP_ERR_INVALID; }
-    if (cfg->rank < 0 || cfg->rank >= n) { set_error("rank out of range"); return PCPP_ERR_INVALID; }
+    const int world = cfg->cfg_split ? 2 * n : n;
+    if (cfg->world != world) { set_error("world (%d) must equal n_patches%s (%d)", cfg->world, cfg->cfg_split ? " x 2 (cfg_split)" : "", world); return PCPP_ERR_INVALID; }
+    if (cfg->rank < 0 || cfg->rank >= world) { set_error("rank out of range"); return PCPP_ERR_INVALID; }
+    if (world > 8) { set_error("PEER backend: at most 8 ranks"); return PCPP_ERR_INVALID; }
   } else if (cfg->comm_backend != PCPP_COMM_LOOPBACK) { set_error("bad comm_backend"); return PCPP_ERR_INVALID; }
   return PCPP_OK;
 }
@@ -89,11 +98,11 @@ struct Builder {
   int rows_at(int level) const { return (P.H >> level) / P.n; }
   int w_at(int level) const { return P.W >> level; }
 
-  int tensor(const std::string& name, int level, int C, int dtype, int pad, int dbl) {
+  int tensor(const std::string& name, int level, int C, int dtype, int pad, int dbl, int B = 0) {
     TDesc t;
     t.name = name; t.level = level; t.rows = rows_at(level); t.W = w_at(level); t.C = C; t.dtype = dtype;
-    t.pad = pad; t.dbl = dbl;
-    t.bytes = (size_t)(t.rows + 2 * pad) * B_CFG * t.W * C * dtype_size(dtype);
+    t.pad = pad; t.dbl = dbl; t.B = B;
+    t.bytes = (size_t)(t.rows + 2 * pad) * (B ? B : P.B) * t.W * C * dtype_size(dtype);
     P.td.push_back(t);
     return (int)P.td.size() - 1;
   }
@@ -232,10 +241,23 @@ struct Builder {
     int tl3 = layernorm(th2, a + ".ln3", level, C);
     long long f1 = take(a + ".ff1.w", {8 * C, C}), f1b = take(a + ".ff1.b", {8 * C});
     long long f2 = take(a + ".ff2.w", {C, 4 * C}), f2b = take(a + ".ff2.b", {C});
+    // W_ff1 = [W_value (4C rows); W_gate (4C rows)] is uploaded in 64-row blocks [value k | gate k], so a
+    // 128-column GEMM tile holds a value column and its gate: the tcgen05 epilogue applies the GEGLU
+    // and writes 4C channels; other paths write the 8C blocked product to tu and run the GEGLU kernel
     int tu = tensor(a + ".ff_u", level, 8 * C, act, 0, 0);
-    { Op& o = op(OP_GEMM); o.in0 = tl3; o.out = tu; o.N = 8 * C; o.w = up_mat(f1, 8LL * C * C); o.b = up_f32(f1b, 8 * C); }
     int tg = tensor(a + ".ff_g", level, 4 * C, act, 0, 0);
-    { Op& o = op(OP_GEGLU); o.in0 = tu; o.out = tg; }
+    {
+      Op& o = op(OP_GEMM); o.in0 = tl3; o.out = tg; o.tmp = tu; o.geglu = 1; o.N = 8 * C;
+      o.w = P.wmat_len; o.b = P.wf32_len;
+      for (int k = 0; k < 4 * C / 64; ++k)
+        for (int half = 0; half < 2; ++half) {            // value block k, then gate block k
+          const long long row0 = (long long)half * 4 * C + 64LL * k;
+          P.uploads.push_back({f1 + row0 * C, 64LL * C, 0, P.wmat_len + (128LL * k + 64 * half) * C});
+          P.uploads.push_back({f1b + row0, 64, 1, P.wf32_len + 128LL * k + 64 * half});
+        }
+      P.wmat_len = (P.wmat_len + 8LL * C * C + 63) & ~63LL;
+      P.wf32_len = (P.wf32_len + 8LL * C + 63) & ~63LL;
+    }
     int th3 = tensor(a + ".fh", level, C, act, 0, 0);
     { Op& o = op(OP_GEMM); o.in0 = tg; o.out = th3; o.N = C; o.w = up_mat(f2, 4LL * C * C); o.b = up_f32(f2b, C); o.res = th2; }
     return th3;
@@ -318,6 +340,12 @@ struct Builder {
       long long wo = take("conv_out.w", {4, 3, 3, P.C0}), bo = take("conv_out.b", {4});
       Op& o = op(OP_CONVOUT); o.in0 = tg; o.out = teps; o.N = 4;
       o.w = up_f32(wo, 4LL * 9 * P.C0); o.w_f32 = 1; o.b = up_f32(bo, 4);
+    }
+    if (P.split) {   // CFG device split: both branches' eps of this patch side by side (the partner's by exchange)
+      int teps2 = tensor("eps2", 0, 4, DT_F32, 0, 0, 2);
+      P.td[teps2].xdst = 1;
+      Op& o = op(OP_EPSX); o.in0 = teps; o.out = teps2;
+      teps = teps2;
     }
     { Op& o = op(OP_CFGDDIM); o.in0 = teps; }
     op(OP_END);

@@ -102,24 +102,24 @@ static void fill_info(Plan& P, pcpp_info* info) {
   }
   for (size_t a = 0; a < P.attns.size() && a < PCPP_MAX_LAYERS; ++a) { info->attn_h[a] = P.attns[a].h; info->attn_r[a] = P.attns[a].r; }
   // closed forms: summed over receiving ranks, one step
-  const long long n = P.n, es = (long long)dtype_size(P.dtype);
+  const long long n = P.n, es = (long long)dtype_size(P.dtype), nb = P.nb;
   if (n > 1) {
     for (const HaloX& hx : P.halos) {
       const TDesc& d = P.td[hx.t];
-      const long long rowb = (long long)B_CFG * d.W * d.C * dtype_size(d.dtype);
-      const long long v = (hx.stride == 1 ? 2 : 1) * (n - 1) * rowb;
+      const long long rowb = (long long)P.B * d.W * d.C * dtype_size(d.dtype);
+      const long long v = nb * (hx.stride == 1 ? 2 : 1) * (n - 1) * rowb;
       info->bytes_async[1] += v; info->bytes_warmup[1] += v; info->bytes_fullmap[1] += v;
     }
     for (const GnX& g : P.gns) {
       (void)g;
-      const long long v = n * (n - 1) * (long long)B_CFG * GN_G * 2 * 8;
+      const long long v = nb * n * (n - 1) * (long long)P.B * GN_G * 2 * 8;
       info->bytes_async[2] += v; info->bytes_warmup[2] += v; info->bytes_fullmap[2] += v;
     }
     for (const AttnX& a : P.attns) {
-      const long long rowb = (long long)B_CFG * a.W * 2 * a.C * es;
-      info->bytes_async[0] += 2 * (n - 1) * a.r * rowb;
-      info->bytes_warmup[0] += (n - 1) * (long long)a.h * n * rowb;
-      info->bytes_fullmap[0] += (n - 1) * (long long)a.h * n * rowb;
+      const long long rowb = (long long)P.B * a.W * 2 * a.C * es;
+      info->bytes_async[0] += nb * 2 * (n - 1) * a.r * rowb;
+      info->bytes_warmup[0] += nb * (n - 1) * (long long)a.h * n * rowb;
+      info->bytes_fullmap[0] += nb * (n - 1) * (long long)a.h * n * rowb;
     }
   }
   compute_ledgers(P, info);
@@ -151,11 +151,12 @@ static pcpp_status setup_plan(Plan& P, int H, int W, int C, int n, double p, int
   if (st != PCPP_OK) return st;
   P.cfg = *cfg; P.H = H; P.W = W; P.C = C; P.n = n; P.p = p; P.warmup = w; P.S = cfg->num_steps;
   P.dtype = cfg->precision == PCPP_FP32 ? DT_F32 : DT_BF16;
-  P.loopback = cfg->comm_backend == PCPP_COMM_LOOPBACK || n == 1;
+  P.split = cfg->cfg_split != 0; P.B = P.split ? 1 : 2; P.nb = P.split ? 2 : 1; P.world = n * P.nb;
+  P.loopback = cfg->comm_backend == PCPP_COMM_LOOPBACK || P.world == 1;
   P.backend = P.loopback ? PCPP_COMM_LOOPBACK : cfg->comm_backend;
   P.xasync = P.loopback && n > 1 && getenv("PCPP_LOOPBACK_ASYNC") && atoi(getenv("PCPP_LOOPBACK_ASYNC")) != 0;
   P.xdelay = (P.xasync && getenv("PCPP_XCH_DELAY")) ? atoll(getenv("PCPP_XCH_DELAY")) : 0;
-  P.nr = P.loopback ? n : 1;
+  P.nr = P.loopback ? P.world : 1;
   P.rank0 = P.loopback ? 0 : cfg->rank;
   return build_program(P, cfg->model);
 }

@@ -81,11 +81,11 @@ size_t plan_memory(Plan& P) {
   std::vector<int> first(nt, 1 << 30), last(nt, -1);
   for (int i = 0; i < (int)P.ops.size(); ++i) {
     const Op& o = P.ops[i];
-    for (int r : {o.in0, o.in1, o.out, o.out2, o.res})
+    for (int r : {o.in0, o.in1, o.out, o.out2, o.res, o.tmp})
       if (r >= 0) { first[r] = std::min(first[r], i); last[r] = std::max(last[r], i); }
   }
   std::vector<char> pinned(nt, 0);
-  for (int t = 0; t < nt; ++t) pinned[t] = P.td[t].dbl || P.td[t].pad || last[t] < 0;
+  for (int t = 0; t < nt; ++t) pinned[t] = P.td[t].dbl || P.td[t].pad || P.td[t].xdst || last[t] < 0;
   for (const HaloX& h : P.halos) pinned[h.t] = 1;
   for (const AttnX& a : P.attns) pinned[a.kv] = 1;
   size_t off = 0;
@@ -130,7 +130,7 @@ size_t plan_memory(Plan& P) {
 
 pcpp_status plan_allocate(Plan& P) {
   size_t off = align256(plan_memory(P));
-  const size_t mb = (size_t)B_CFG * GN_G * 2 * sizeof(double);
+  const size_t mb = (size_t)P.B * GN_G * 2 * sizeof(double);
   for (auto& g : P.gns) {
     for (int q = 0; q < 2; ++q) { g.off_m[q] = off; off = align256(off + mb); }
     for (int q = 0; q < 2; ++q) { g.off_mall[q] = off; off = align256(off + mb * P.n); }
@@ -154,7 +154,7 @@ pcpp_status plan_allocate(Plan& P) {
   size_t gat_level[3] = {0, 0, 0};
   bool have_level[3] = {false, false, false};
   for (auto& a : P.attns) {
-    const size_t rowb = (size_t)B_CFG * a.W * 2 * a.C * es;
+    const size_t rowb = (size_t)P.B * a.W * 2 * a.C * es;
     for (int q = 0; q < 2; ++q) {
       a.off_top[q] = off; off = align256(off + std::max<size_t>(16, (size_t)a.r * rowb));
       a.off_bot[q] = off; off = align256(off + std::max<size_t>(16, (size_t)a.r * rowb));
@@ -203,7 +203,7 @@ pcpp_status plan_allocate(Plan& P) {
     for (const Op& o : P.ops)
       if (o.k == OP_CONV || o.k == OP_GEMM) {
         const TDesc& t = P.td[o.out];
-        mx = std::max(mx, (size_t)t.rows * B_CFG * t.W * (size_t)o.N);
+        mx = std::max(mx, (size_t)t.rows * P.B * t.W * (size_t)o.N);
       }
     P.ws_elems = std::min<size_t>(8 * mx, (size_t)1 << 28);
     P.ws = (float*)galloc(P.ws_elems * 4);
@@ -211,8 +211,8 @@ pcpp_status plan_allocate(Plan& P) {
   if (P.xf) {     // cross-attention context: as given, laid out per level, and every layer's keys/values
     P.ctx_f32 = (float*)galloc((size_t)2 * 77 * P.ctx_dim * 4);
     for (int l = 0; l < P.levels; ++l)
-      P.ctx_level[l] = galloc((size_t)P.ctx_rows(l) * B_CFG * (P.W >> l) * P.ctx_dim * es);
-    for (auto& xa : P.xattns) xa.kv = galloc((size_t)P.ctx_rows(xa.level) * B_CFG * (P.W >> xa.level) * 2 * xa.C * es);
+      P.ctx_level[l] = galloc((size_t)P.ctx_rows(l) * 2 * (P.W >> l) * P.ctx_dim * es);
+    for (auto& xa : P.xattns) xa.kv = galloc((size_t)P.ctx_rows(xa.level) * 2 * (P.W >> xa.level) * 2 * xa.C * es);
   }
   for (void* p : P.gallocs) if (!p) { set_error("cudaMalloc failed for global buffers"); return PCPP_ERR_OOM; }
   // DDIM schedule (reading D2): scaled_linear betas, 'leading' spacing, offset 1, final ab_prev = ab[0]
@@ -305,9 +305,10 @@ pcpp_status plan_upload_weights(Plan& P, const float* blob) {
 static ActView view(const Plan& P, int vr, int t, int par) {
   const TDesc& d = P.td[t];
   ActView v;
-  const size_t rowb = (size_t)B_CFG * d.W * d.C * dtype_size(d.dtype);
+  const int B = d.B ? d.B : P.B;
+  const size_t rowb = (size_t)B * d.W * d.C * dtype_size(d.dtype);
   v.base = P.rm[vr].arena + d.off[d.dbl ? par : 0] + (size_t)d.pad * rowb;
-  v.rows = d.rows; v.B = B_CFG; v.W = d.W; v.C = d.C; v.dtype = d.dtype;
+  v.rows = d.rows; v.B = B; v.W = d.W; v.C = d.C; v.dtype = d.dtype;
   return v;
 }
 
@@ -329,10 +330,12 @@ static char* resolve(const Plan& P, int vr, const BufRef& r) {
 // ---------------------------------------------------------------------------------------------
 static BufRef tref(const Plan& P, int t, int par, int row) {
   const TDesc& d = P.td[t];
-  const long long rowb = (long long)B_CFG * d.W * d.C * dtype_size(d.dtype);
+  const long long rowb = (long long)(d.B ? d.B : P.B) * d.W * d.C * dtype_size(d.dtype);
   return BufRef{BK_TENSOR, t, par, (long long)(row + d.pad) * rowb};
 }
 
+// Transfers of one exchange point.  Ranks are global (P.grank(branch, patch)); buffer offsets use
+// the patch index within the branch group (a group exchanges only among its own patches).
 static XGroup make_group(const Plan& P, const Op& op, int sync, int par, std::vector<Xfer>& lb) {
   XGroup G;
   const int n = P.n;
@@ -341,71 +344,97 @@ static XGroup make_group(const Plan& P, const Op& op, int sync, int par, std::ve
   if (op.k == OP_HALO) {
     const HaloX& hx = P.halos[op.xid];
     const TDesc& d = P.td[hx.t];
-    const size_t rowb = (size_t)B_CFG * d.W * d.C * dtype_size(d.dtype);
+    const size_t rowb = (size_t)P.B * d.W * d.C * dtype_size(d.dtype);
     const int h = d.rows, pd = sync ? par : 1 - par;
     G.cls = 1;
-    for (int i = 0; i < n; ++i) {
-      if (i > 0) {   // my top halo <- rank i-1's last row
-        Xfer x{1, i - 1, i, tref(P, hx.t, par, h - 1), tref(P, hx.t, pd, -1), rowb};
-        G.remote.push_back(x); lb.push_back(x);
-        if (sync) { G.local.push_back({1, i, i, tref(P, hx.t, par, -1), tref(P, hx.t, 1 - par, -1), rowb});
-                    lb.push_back({1, i - 1, i, tref(P, hx.t, par, h - 1), tref(P, hx.t, 1 - par, -1), rowb}); }
+    for (int bq = 0; bq < P.nb; ++bq)
+      for (int i = 0; i < n; ++i) {
+        const int me = P.grank(bq, i);
+        if (i > 0) {   // my top halo <- patch i-1's last row
+          const int src = P.grank(bq, i - 1);
+          Xfer x{1, src, me, tref(P, hx.t, par, h - 1), tref(P, hx.t, pd, -1), rowb};
+          G.remote.push_back(x); lb.push_back(x);
+          if (sync) { G.local.push_back({1, me, me, tref(P, hx.t, par, -1), tref(P, hx.t, 1 - par, -1), rowb});
+                      lb.push_back({1, src, me, tref(P, hx.t, par, h - 1), tref(P, hx.t, 1 - par, -1), rowb}); }
+        }
+        if (i < n - 1 && hx.stride == 1) {   // my bottom halo <- patch i+1's first row
+          const int src = P.grank(bq, i + 1);
+          Xfer x{1, src, me, tref(P, hx.t, par, 0), tref(P, hx.t, pd, h), rowb};
+          G.remote.push_back(x); lb.push_back(x);
+          if (sync) { G.local.push_back({1, me, me, tref(P, hx.t, par, h), tref(P, hx.t, 1 - par, h), rowb});
+                      lb.push_back({1, src, me, tref(P, hx.t, par, 0), tref(P, hx.t, 1 - par, h), rowb}); }
+        }
       }
-      if (i < n - 1 && hx.stride == 1) {   // my bottom halo <- rank i+1's first row
-        Xfer x{1, i + 1, i, tref(P, hx.t, par, 0), tref(P, hx.t, pd, h), rowb};
-        G.remote.push_back(x); lb.push_back(x);
-        if (sync) { G.local.push_back({1, i, i, tref(P, hx.t, par, h), tref(P, hx.t, 1 - par, h), rowb});
-                    lb.push_back({1, i + 1, i, tref(P, hx.t, par, 0), tref(P, hx.t, 1 - par, h), rowb}); }
-      }
-    }
   } else if (op.k == OP_GN) {
-    const size_t mb = (size_t)B_CFG * GN_G * 2 * sizeof(double);
+    const size_t mb = (size_t)P.B * GN_G * 2 * sizeof(double);
     G.cls = 2; G.allgather = 1;
     G.ag_send = BufRef{BK_GNM, op.xid, par, 0};
     G.ag_recv = BufRef{BK_GNMALL, op.xid, par, 0};
     G.ag_bytes = mb;
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j < n; ++j) {
-        Xfer x{2, j, i, BufRef{BK_GNM, op.xid, par, 0}, BufRef{BK_GNMALL, op.xid, par, (long long)(j * mb)}, mb};
-        if (i != j) G.remote.push_back(x);
-        lb.push_back(x);
-      }
+    for (int bq = 0; bq < P.nb; ++bq)
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+          Xfer x{2, P.grank(bq, j), P.grank(bq, i), BufRef{BK_GNM, op.xid, par, 0},
+                 BufRef{BK_GNMALL, op.xid, par, (long long)(j * mb)}, mb};
+          if (i != j) G.remote.push_back(x);
+          lb.push_back(x);
+        }
   } else if (op.k == OP_KVX) {
     const AttnX& a = P.attns[op.xid];
     const TDesc& d = P.td[a.kv];
-    const size_t rowb = (size_t)B_CFG * d.W * d.C * dtype_size(d.dtype);
+    const size_t rowb = (size_t)P.B * d.W * d.C * dtype_size(d.dtype);
     const int h = a.h, r = a.r;
     G.cls = 0;
     const bool fullmap = P.cfg.scheme == PCPP_SCHEME_FULLMAP;
-    if (!sync && !fullmap) {            // PCPP async: only the p-fraction bands, p2p to i +- 1
-      for (int i = 0; i < n && r > 0; ++i) {
-        if (i > 0) { Xfer x{0, i - 1, i, tref(P, a.kv, par, h - r), BufRef{BK_TOP, op.xid, par, 0}, r * rowb}; G.remote.push_back(x); lb.push_back(x); }
-        if (i < n - 1) { Xfer x{0, i + 1, i, tref(P, a.kv, par, 0), BufRef{BK_BOT, op.xid, par, 0}, r * rowb}; G.remote.push_back(x); lb.push_back(x); }
-      }
-    } else {                            // all-gather of the full map (warm-up, or DistriFusion)
-      const int gp = fullmap ? par : 0;
-      G.allgather = 1;
-      G.ag_send = tref(P, a.kv, par, 0);
-      G.ag_recv = BufRef{BK_GAT, op.xid, gp, 0};
-      G.ag_bytes = (size_t)h * rowb;
-      for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) {
-          Xfer x{0, j, i, tref(P, a.kv, par, 0), BufRef{BK_GAT, op.xid, gp, (long long)((size_t)j * h * rowb)}, (size_t)h * rowb};
-          if (i != j) { G.remote.push_back(x); lb.push_back(x); }
+    for (int bq = 0; bq < P.nb; ++bq) {
+      auto R = [&](int i) { return P.grank(bq, i); };
+      if (!sync && !fullmap) {            // PCPP async: only the p-fraction bands, p2p to i +- 1
+        for (int i = 0; i < n && r > 0; ++i) {
+          if (i > 0) { Xfer x{0, R(i - 1), R(i), tref(P, a.kv, par, h - r), BufRef{BK_TOP, op.xid, par, 0}, r * rowb}; G.remote.push_back(x); lb.push_back(x); }
+          if (i < n - 1) { Xfer x{0, R(i + 1), R(i), tref(P, a.kv, par, 0), BufRef{BK_BOT, op.xid, par, 0}, r * rowb}; G.remote.push_back(x); lb.push_back(x); }
         }
-      if (!fullmap && r > 0) {          // warm-up seeds the band buffers for step k+1 (unpack)
-        for (int i = 0; i < n; ++i) {
-          if (i > 0) {
-            G.local.push_back({0, i, i, BufRef{BK_GAT, op.xid, 0, (long long)((size_t)(i * h - r) * rowb)}, BufRef{BK_TOP, op.xid, par, 0}, r * rowb});
-            lb.push_back({0, i - 1, i, tref(P, a.kv, par, h - r), BufRef{BK_TOP, op.xid, par, 0}, r * rowb});
+      } else {                            // all-gather of the full map (warm-up, or DistriFusion)
+        const int gp = fullmap ? par : 0;
+        G.allgather = 1;
+        G.ag_send = tref(P, a.kv, par, 0);
+        G.ag_recv = BufRef{BK_GAT, op.xid, gp, 0};
+        G.ag_bytes = (size_t)h * rowb;
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) {
+            Xfer x{0, R(j), R(i), tref(P, a.kv, par, 0), BufRef{BK_GAT, op.xid, gp, (long long)((size_t)j * h * rowb)}, (size_t)h * rowb};
+            if (i != j) { G.remote.push_back(x); lb.push_back(x); }
           }
-          if (i < n - 1) {
-            G.local.push_back({0, i, i, BufRef{BK_GAT, op.xid, 0, (long long)((size_t)((i + 1) * h) * rowb)}, BufRef{BK_BOT, op.xid, par, 0}, r * rowb});
-            lb.push_back({0, i + 1, i, tref(P, a.kv, par, 0), BufRef{BK_BOT, op.xid, par, 0}, r * rowb});
+        if (!fullmap && r > 0) {          // warm-up seeds the band buffers for step k+1 (unpack)
+          for (int i = 0; i < n; ++i) {
+            if (i > 0) {
+              G.local.push_back({0, R(i), R(i), BufRef{BK_GAT, op.xid, 0, (long long)((size_t)(i * h - r) * rowb)}, BufRef{BK_TOP, op.xid, par, 0}, r * rowb});
+              lb.push_back({0, R(i - 1), R(i), tref(P, a.kv, par, h - r), BufRef{BK_TOP, op.xid, par, 0}, r * rowb});
+            }
+            if (i < n - 1) {
+              G.local.push_back({0, R(i), R(i), BufRef{BK_GAT, op.xid, 0, (long long)((size_t)((i + 1) * h) * rowb)}, BufRef{BK_BOT, op.xid, par, 0}, r * rowb});
+              lb.push_back({0, R(i + 1), R(i), tref(P, a.kv, par, 0), BufRef{BK_BOT, op.xid, par, 0}, r * rowb});
+            }
           }
         }
       }
     }
+  } else if (op.k == OP_EPSX) {
+    // CFG device split: the partner (same patch, other branch) sends its eps rows into my
+    // two-branch buffer eps2 [h][2][W][4]; my own rows go to my slot.  Needed in the same step
+    // (synchronous every step, like DistriFusion's), then every rank applies CFG + DDIM itself.
+    const TDesc& e = P.td[op.in0];
+    const size_t row1 = (size_t)e.W * 4 * sizeof(float);
+    G.cls = 3; G.wait = 1;
+    for (int bq = 0; bq < 2; ++bq)
+      for (int i = 0; i < n; ++i) {
+        const int me = P.grank(bq, i), pa = P.grank(1 - bq, i);
+        for (int r = 0; r < e.rows; ++r) {
+          const BufRef own{BK_TENSOR, op.in0, par, (long long)(r * row1)};
+          Xfer x{3, pa, me, own, BufRef{BK_TENSOR, op.out, par, (long long)((2 * r + 1 - bq) * row1)}, row1};
+          G.remote.push_back(x); lb.push_back(x);
+          lb.push_back({3, me, me, own, BufRef{BK_TENSOR, op.out, par, (long long)((2 * r + bq) * row1)}, row1});
+        }
+      }
   }
   return G;
 }
@@ -419,7 +448,7 @@ pcpp_status plan_build_exchanges(Plan& P) {
   int nx = 0;
   for (size_t i = 0; i < P.ops.size(); ++i) {
     const OpK k = P.ops[i].k;
-    if ((k == OP_HALO || k == OP_KVX || k == OP_GN) && P.n > 1) P.op_xord[i] = nx++;
+    if (((k == OP_HALO || k == OP_KVX || k == OP_GN) && P.n > 1) || k == OP_EPSX) P.op_xord[i] = nx++;
   }
   std::vector<CopySeg> host;
   std::vector<Xfer> lb;
@@ -465,9 +494,15 @@ pcpp_status plan_build_exchanges(Plan& P) {
 void compute_ledgers(Plan& P, pcpp_info* info) {
   std::vector<Xfer> lb;
   for (int c = 0; c < 3; ++c) { info->bytes_counted_async[c] = 0; info->bytes_counted_warmup[c] = 0; }
-  if (P.n == 1) return;
+  info->bytes_eps = 0;
+  if (P.world == 1) return;
   for (const Op& op : P.ops) {
-    if (op.k != OP_HALO && op.k != OP_KVX && op.k != OP_GN) continue;
+    if (op.k == OP_EPSX) {
+      XGroup G = make_group(P, op, 0, 0, lb);
+      for (auto& x : G.remote) info->bytes_eps += (long long)x.bytes;
+      continue;
+    }
+    if ((op.k != OP_HALO && op.k != OP_KVX && op.k != OP_GN) || P.n == 1) continue;
     for (int sync = 0; sync < 2; ++sync) {
       XGroup G = make_group(P, op, sync, 0, lb);
       for (auto& x : G.remote) (sync ? info->bytes_counted_warmup : info->bytes_counted_async)[x.cls] += (long long)x.bytes;
@@ -499,7 +534,7 @@ void peer_barrier(Plan& P, cudaStream_t s) { launch_peer_barrier(P.bar, s); }
 pcpp_status plan_peer_connect(Plan& P, const void* handles) {
   if (P.backend != PCPP_COMM_PEER) { set_error("pcpp_peer_connect: plan does not use the PEER backend"); return PCPP_ERR_STATE; }
   if (P.peer_connected) { set_error("pcpp_peer_connect: already connected"); return PCPP_ERR_STATE; }
-  const int me = P.rank0, n = P.n;
+  const int me = P.rank0, n = P.world;
   char* own = P.rm[0].arena;
   const cudaIpcMemHandle_t* hs = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
   for (int j = 0; j < n; ++j) {
@@ -528,12 +563,14 @@ pcpp_status plan_peer_connect(Plan& P, const void* handles) {
         P.seg_push[sync][par][xo] = sr;
       }
     }
-  {   // final gather: my latent patch into row block `me` of every rank's x0g
-    const size_t pb = (size_t)(P.H / n) * P.W * 4 * sizeof(float);
+  {   // final gather: my latent patch into row block `patch` of every rank's x0g (with the CFG split
+      // both branches hold the same patch; branch 0 sends it)
+    const size_t pb = (size_t)(P.H / P.n) * P.W * 4 * sizeof(float);
     P.seg_x0.first = (int)host.size();
-    for (int j = 0; j < n; ++j)
-      host.push_back(CopySeg{own + P.off_lat, P.peer_base[j] + P.off_x0g + (size_t)me * pb, (unsigned long long)pb});
-    P.seg_x0.count = n; P.seg_x0.maxb = pb;
+    if (P.branch_of(me) == 0)
+      for (int j = 0; j < n; ++j)
+        host.push_back(CopySeg{own + P.off_lat, P.peer_base[j] + P.off_x0g + (size_t)P.patch_of(me) * pb, (unsigned long long)pb});
+    P.seg_x0.count = (int)host.size() - P.seg_x0.first; P.seg_x0.maxb = pb;
   }
   CK(cudaMalloc(&P.push_dev, std::max<size_t>(1, host.size()) * sizeof(CopySeg)));
   CK(cudaMemcpy(P.push_dev, host.data(), host.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
@@ -549,7 +586,8 @@ pcpp_status plan_peer_connect(Plan& P, const void* handles) {
 
 static pcpp_status exchange(Plan& P, int xo, int sync, int par) {
   const XGroup& G = P.xg[sync][par][xo];
-  if (P.comm_off && !sync) return PCPP_OK;
+  const bool now = sync || G.wait;        // consumed in this step (warm-up, or the CFG-split eps exchange)
+  if (P.comm_off && !now) return PCPP_OK;
   if (P.loopback && P.xasync) {     // the NCCL protocol with device copies (test mode)
     const auto& sr = P.seg_remote[sync][par][xo];
     CK(cudaEventRecord(P.ev_x, P.s0));
@@ -575,7 +613,7 @@ static pcpp_status exchange(Plan& P, int xo, int sync, int par) {
     // an all-gather of attention K/V first waits until every peer has left the previous attention
     // layer (the gather buffer is shared by the layers of a level).
     const auto& sr = P.seg_push[sync][par][xo];
-    if (!sync) {
+    if (!now) {
       CK(cudaEventRecord(P.ev_x, P.s0));
       CK(cudaStreamWaitEvent(P.s1, P.ev_x, 0));
       launch_copy_segments(P.push_dev + sr.first, sr.count, sr.maxb, P.s1);
@@ -640,7 +678,7 @@ static unsigned op_kind(OpK k) {
     case OP_CONV: case OP_GEMM: return K_GEMM;
     case OP_ATTN: return K_ATTN;
     case OP_GN: return K_GN;
-    case OP_HALO: case OP_KVX: return K_XCH;
+    case OP_HALO: case OP_KVX: case OP_EPSX: return K_XCH;
     case OP_XATTN: return K_ATTN;
     case OP_END: return K_END;
     default: return K_MISC;
@@ -671,7 +709,7 @@ pcpp_status plan_autotune(Plan& P) {
     g.taps = op.k == OP_CONV ? 9 : 1;
     g.stride = op.stride;
     const ActView o = view(P, 0, op.out, 0);
-    g.rows_out = o.rows; g.w_out = o.W; g.B = B_CFG;
+    g.rows_out = o.rows; g.w_out = o.W; g.B = P.B;
     g.w = op.w_f32 ? (const void*)(P.wf32 + op.w) : (const void*)(wm + (size_t)op.w * es);
     g.wdtype = op.w_f32 ? DT_F32 : P.dtype;
     g.N = op.N;
@@ -680,6 +718,7 @@ pcpp_status plan_autotune(Plan& P) {
     if (op.res >= 0) g.res = view(P, 0, op.res, 0);
     g.out = o;
     if (op.out2 >= 0) { g.out2 = view(P, 0, op.out2, 0); g.n_split = op.n_split; }
+    g.geglu = op.geglu;
     g.ws = P.ws; g.ws_elems = P.ws_elems;
     int slots = 0;
     if (op.gn_fuse >= 0) { g.gn_part = reinterpret_cast<double*>(P.rm[0].arena + P.off_epart); g.gn_slots = &slots; }
@@ -725,7 +764,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
   const long long fb0 = simt_fallback_count();
   // PEER: every peer has finished step k-1 (its compute and its pushes) before this step reads what
   // they pushed during k-1 and before this step pushes into the buffers they read during k-1
-  if (P.backend == PCPP_COMM_PEER && n > 1 && (mask & K_XCH)) {
+  if (P.backend == PCPP_COMM_PEER && P.world > 1 && (mask & K_XCH)) {
     if (!P.peer_connected) { set_error("PEER backend: pcpp_peer_connect has not been called"); return PCPP_ERR_STATE; }
     peer_barrier(P, s);
     P.launches_per_step += 1;
@@ -751,7 +790,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
       case OP_PREP: {
         const int h = P.H / n;
         for (int vr = 0; vr < nr; ++vr) {
-          const float* lat = latent + (P.loopback ? (size_t)vr * h * P.W * 4 : 0);
+          const float* lat = latent + (P.loopback ? (size_t)P.patch_of(vr) * h * P.W * 4 : 0);
           launch_prep_latent(lat, view(P, vr, op.out, par), s);
         }
         P.launches_per_step += nr;
@@ -759,6 +798,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
       }
       case OP_HALO:
       case OP_KVX:
+      case OP_EPSX:
         if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
         break;
       case OP_CONV:
@@ -771,12 +811,13 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           g.taps = op.k == OP_CONV ? 9 : 1;
           g.stride = op.stride;
           const ActView o = view(P, vr, op.out, par);
-          g.rows_out = o.rows; g.w_out = o.W; g.B = B_CFG;
+          g.rows_out = o.rows; g.w_out = o.W; g.B = P.B;
           g.w = op.w_f32 ? (const void*)(P.wf32 + op.w) : (const void*)(wm + (size_t)op.w * es);
           g.wdtype = op.w_f32 ? DT_F32 : P.dtype;
           g.N = op.N;
           g.bias = op.b >= 0 ? P.wf32 + op.b : nullptr;
-          if (op.temb_off >= 0) { g.temb = P.tproj + op.temb_off; g.temb_ld = P.J; }
+          // temb rows [2][J]: batch b of this rank is CFG branch b, or the rank's branch with the split
+          if (op.temb_off >= 0) { g.temb = P.tproj + op.temb_off + (size_t)P.branch_of(P.rank0 + vr) * P.J; g.temb_ld = P.J; }
           if (op.res >= 0) g.res = view(P, vr, op.res, par);
           g.out = o;
           if (op.out2 >= 0) { g.out2 = view(P, vr, op.out2, par); g.n_split = op.n_split; }
@@ -784,6 +825,16 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           if (op.gn_fuse >= 0) {
             g.gn_part = reinterpret_cast<double*>(P.rm[vr].arena + P.off_epart);
             g.gn_slots = &P.gn_slots[(size_t)vr * P.gns.size() + op.gn_fuse];
+          }
+          if (op.geglu) {    // fused GEGLU epilogue on the tensor-core path, else GEMM into tmp + GEGLU kernel
+            g.geglu = 1;
+            if (!(P.use_tc && gemm_tc_supported(g))) {
+              g.geglu = 0;
+              g.out = view(P, vr, op.tmp, par);
+              launch_gemm_tc_or_simt(P, g, s);
+              launch_geglu(g.out, o, s);
+              continue;
+            }
           }
           launch_gemm_tc_or_simt(P, g, s);
         }
@@ -837,14 +888,14 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
       case OP_ATTN: {
         const AttnX& ax = P.attns[op.xid];
         const TDesc& kvd = P.td[ax.kv];
-        const size_t rowb = (size_t)B_CFG * kvd.W * kvd.C * es;
+        const size_t rowb = (size_t)P.B * kvd.W * kvd.C * es;
         const bool fullmap = P.cfg.scheme == PCPP_SCHEME_FULLMAP;
         for (int vr = 0; vr < nr; ++vr) {
-          const int i = P.rank0 + vr;
+          const int i = P.patch_of(P.rank0 + vr);
           char* base = P.rm[vr].arena;
           AttnArgs a;
           a.q = view(P, vr, op.in0, par).base;
-          a.h = ax.h; a.B = B_CFG; a.W = ax.W; a.C = ax.C; a.dtype = P.dtype;
+          a.h = ax.h; a.B = P.B; a.W = ax.W; a.C = ax.C; a.dtype = P.dtype;
           a.out = view(P, vr, op.out, par).base;
           const void* local = view(P, vr, op.in1, par).base;
           int ns = 0;
@@ -875,16 +926,12 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           }
         P.launches_per_step += nr;
         break;
-      case OP_GEGLU:
-        for (int vr = 0; vr < nr; ++vr) launch_geglu(view(P, vr, op.in0, par), view(P, vr, op.out, par), s);
-        P.launches_per_step += nr;
-        break;
       case OP_XATTN: {     // cross-attention: queries of the patch, keys/values of the 77-token context
         const XAttnX& xa = P.xattns[op.xid];
         for (int vr = 0; vr < nr; ++vr) {
           const ActView q = view(P, vr, op.in0, par);
           AttnArgs a;
-          a.q = q.base; a.h = q.rows; a.B = B_CFG; a.W = q.W; a.C = xa.C; a.dtype = P.dtype;
+          a.q = q.base; a.h = q.rows; a.B = P.B; a.W = q.W; a.C = xa.C; a.dtype = P.dtype;
           a.out = view(P, vr, op.out, par).base;
           a.src[0] = AttnSrc{xa.kv, P.ctx_rows(xa.level), 77};
           a.nsrc = 1;
@@ -906,10 +953,12 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
       case OP_CFGDDIM: {
         const int h = P.H / n;
         for (int vr = 0; vr < nr; ++vr) {
-          float* lat = latent + (P.loopback ? (size_t)vr * h * P.W * 4 : 0);
+          // CFG split in one process: both branches of a patch compute the same update; branch 0 writes it
+          if (P.loopback && P.branch_of(vr) == 1) continue;
+          float* lat = latent + (P.loopback ? (size_t)P.patch_of(vr) * h * P.W * 4 : 0);
           if (P.cfg.scheduler == PCPP_SCHED_ANCESTRAL)
             launch_cfg_ancestral(reinterpret_cast<const float*>(view(P, vr, op.in0, par).base), lat, h, P.W,
-                                 (P.rank0 + vr) * h, P.cfg.guidance_scale, P.coef_anc, P.cfg.noise_seed, P.k_dev, s);
+                                 P.patch_of(P.rank0 + vr) * h, P.cfg.guidance_scale, P.coef_anc, P.cfg.noise_seed, P.k_dev, s);
           else if (P.cfg.scheduler == PCPP_SCHED_DPMPP2M)
             launch_cfg_dpmpp(reinterpret_cast<const float*>(view(P, vr, op.in0, par).base), lat,
                              P.x0_hist + (size_t)vr * h * P.W * 4, h, P.W, P.cfg.guidance_scale, P.coef_dpm, P.k_dev, s);
@@ -954,7 +1003,7 @@ void print_op_timing(Plan& P, float* latent, int sync, int par) {
     if (op.k == OP_CONV || op.k == OP_GEMM) {
       const TDesc& o = P.td[op.out];
       const int cin = P.td[op.in0].C + (op.in1 >= 0 ? P.td[op.in1].C : 0);
-      const double fl = 2.0 * o.rows * B_CFG * o.W * op.N * (op.k == OP_CONV ? 9 : 1) * cin * P.nr;
+      const double fl = 2.0 * o.rows * P.B * o.W * op.N * (op.k == OP_CONV ? 9 : 1) * cin * P.nr;
       fprintf(stderr, "op %3zu %-4s rows=%3d W=%3d N=%4d cin=%4d s=%d res=%d gn=%d out2=%d %8.1f us %6.0f TF/s\n", oi,
               names[k], o.rows, o.W, op.N, cin, op.stride, op.res >= 0, op.gn_fuse >= 0, op.out2 >= 0, ms * 1e3,
               fl / (ms * 1e-3) / 1e12);
@@ -976,9 +1025,9 @@ void op_work(const Plan& P, unsigned kind, int sync, double* flops, double* byte
     if (!(op_kind(op.k) & kind)) continue;
     switch (op.k) {
       case OP_CONV: case OP_GEMM: {
-        const TDesc& o = P.td[op.out];
+        const TDesc& o = P.td[op.geglu ? op.tmp : op.out];
         double cin = P.td[op.in0].C + (op.in1 >= 0 ? P.td[op.in1].C : 0);
-        const double M = (double)o.rows * B_CFG * o.W;
+        const double M = (double)o.rows * P.B * o.W;
         f += 2.0 * M * op.N * (op.k == OP_CONV ? 9 : 1) * cin * P.nr;
         nl += P.nr;
         break;
@@ -986,14 +1035,14 @@ void op_work(const Plan& P, unsigned kind, int sync, double* flops, double* byte
       case OP_ATTN: {
         const AttnX& a = P.attns[op.xid];
         for (int vr = 0; vr < P.nr; ++vr) {
-          const int i = P.rank0 + vr;
+          const int i = P.patch_of(P.rank0 + vr);
           int kv = a.h;
           if (n > 1) {
             if (sync || P.cfg.scheme == PCPP_SCHEME_FULLMAP) kv = a.h * n;
             else kv = a.h + (i > 0 ? a.r : 0) + (i < n - 1 ? a.r : 0);
           }
-          f += 4.0 * ((double)a.h * a.W) * ((double)kv * a.W) * a.C * B_CFG;
-          by += ((double)a.h * a.W * a.C * 2 + (double)kv * a.W * 2 * a.C) * B_CFG * es;   // Q + O + K/V
+          f += 4.0 * ((double)a.h * a.W) * ((double)kv * a.W) * a.C * P.B;
+          by += ((double)a.h * a.W * a.C * 2 + (double)kv * a.W * 2 * a.C) * P.B * es;   // Q + O + K/V
         }
         nl += P.nr;
         break;
@@ -1001,15 +1050,15 @@ void op_work(const Plan& P, unsigned kind, int sync, double* flops, double* byte
       case OP_XATTN: {
         const XAttnX& xa = P.xattns[op.xid];
         const TDesc& q = P.td[op.in0];
-        f += 4.0 * ((double)q.rows * q.W) * 77.0 * xa.C * B_CFG * P.nr;
-        by += ((double)q.rows * q.W * xa.C * 2 + 77.0 * 2 * xa.C) * B_CFG * es * P.nr;
+        f += 4.0 * ((double)q.rows * q.W) * 77.0 * xa.C * P.B * P.nr;
+        by += ((double)q.rows * q.W * xa.C * 2 + 77.0 * 2 * xa.C) * P.B * es * P.nr;
         nl += P.nr;
         break;
       }
       case OP_GN: {
         const TDesc& x = P.td[op.in0];
         double C = x.C + (op.in1 >= 0 ? P.td[op.in1].C : 0);
-        by += 3.0 * x.rows * B_CFG * x.W * C * es * P.nr;     // stats read + apply read/write
+        by += 3.0 * x.rows * P.B * x.W * C * es * P.nr;     // stats read + apply read/write
         nl += 2 * P.nr;
         break;
       }

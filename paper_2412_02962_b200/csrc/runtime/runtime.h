@@ -18,15 +18,17 @@ constexpr int B_CFG = 2;
 struct TDesc {
   std::string name;
   int level = 0, rows = 0, W = 0, C = 0, dtype = 0;
+  int B = 0;         // batch of the tensor (0: the plan's batch per rank, P.B)
   int pad = 0;       // 1: rows -1 and `rows` exist (conv halo rows, zero at image borders)
   int dbl = 0;       // 1: one buffer per step parity (its rows are sent to neighbours)
+  int xdst = 0;      // 1: written by other ranks inside a step (own memory range, never shared)
   size_t bytes = 0;  // per parity, including halo rows
   size_t off[2] = {0, 0};   // offsets in the rank arena
 };
 
 // ---- ops ------------------------------------------------------------------------------------------
 enum OpK { OP_TEMB, OP_PREP, OP_HALO, OP_CONV, OP_GEMM, OP_GN, OP_KVX, OP_ATTN, OP_UPS, OP_CONVOUT,
-           OP_CFGDDIM, OP_END, OP_LN, OP_GEGLU, OP_XATTN };
+           OP_CFGDDIM, OP_END, OP_LN, OP_GEGLU, OP_XATTN, OP_EPSX };
 
 struct Op {
   OpK k;
@@ -40,6 +42,8 @@ struct Op {
   int xid = -1;             // exchange id (halo / gn / attn index)
   int N = 0;                // output channels for GEMM/CONV
   int gn_fuse = -1;         // GEMM/CONV: GroupNorm index whose statistics its epilogue produces
+  int geglu = 0;            // GEMM: GEGLU epilogue (out has N/2 channels); tmp = the [.., N] fallback tensor
+  int tmp = -1;
 };
 
 // ---- exchange buffers --------------------------------------------------------------------------
@@ -77,7 +81,16 @@ struct Plan {
   pcpp_config cfg{};
   int dtype = DT_BF16;
   int levels = 1, C0 = 128, T = 512, SIN = 128;
-  int nr = 1;            // virtual ranks held here (n for loopback, 1 for NCCL)
+  int nr = 1;            // virtual ranks held here (world for loopback, 1 for NCCL / PEER)
+  // CFG device split (cfg_split, §2.2): 2 groups of n ranks, group b runs CFG
+  // branch b (b = 0 uncond, 1 cond) as batch 1 over the n patches; rank r = b * n + patch
+  bool split = false;
+  int B = 2;             // CFG batch per rank (2, or 1 with the split)
+  int nb = 1;            // branch groups (2 with the split)
+  int world = 1;         // n * nb
+  int patch_of(int r) const { return r % n; }
+  int branch_of(int r) const { return split ? r / n : 0; }
+  int grank(int b, int i) const { return b * n + i; }
   int rank0 = 0;         // global rank of virtual rank 0
   bool loopback = true;
   // loopback test mode (PCPP_LOOPBACK_ASYNC=1): the exchange copies run on the comm stream S1 with the

@@ -34,7 +34,7 @@ class pcpp_config(C.Structure):
                 ("model", C.c_int), ("weights", C.POINTER(C.c_float)), ("weights_len", C.c_size_t),
                 ("nccl_id", C.c_void_p), ("stream", C.c_void_p), ("comm_backend", C.c_int),
                 ("kernels", C.c_int), ("use_graphs", C.c_int), ("scheduler", C.c_int),
-                ("noise_seed", C.c_ulonglong)]
+                ("noise_seed", C.c_ulonglong), ("cfg_split", C.c_int)]
 
 
 class pcpp_info(C.Structure):
@@ -46,7 +46,8 @@ class pcpp_info(C.Structure):
                 ("device_bytes", C.c_longlong), ("n_kernels_per_step", C.c_int), ("graphs", C.c_int),
                 ("tc_kernels", C.c_int), ("step_flops", C.c_double), ("step_flops_rank_max", C.c_double),
                 ("arena_bytes_per_rank", C.c_longlong), ("arena_bytes_unplanned", C.c_longlong),
-                ("simt_fallbacks", C.c_int), ("backend", C.c_int), ("comm_lib", C.c_char * 192)]
+                ("simt_fallbacks", C.c_int), ("backend", C.c_int), ("comm_lib", C.c_char * 192),
+                ("bytes_eps", C.c_longlong)]
 
     def as_dict(self):
         d = {}
@@ -172,7 +173,7 @@ def pcpp_get_unique_id() -> bytes:
 
 def make_config(model="sdxl", num_steps=50, guidance=5.0, precision="bf16", scheme="pcpp",
                 backend="loopback", rank=0, world=1, weights=None, nccl_id=None, stream=None,
-                kernels="auto", graphs=True, scheduler="ddim", noise_seed=0):
+                kernels="auto", graphs=True, scheduler="ddim", noise_seed=0, cfg_split=False):
     cfg = pcpp_config()
     lib().pcpp_config_default(C.byref(cfg))
     cfg.model = MODELS[model]
@@ -186,6 +187,7 @@ def make_config(model="sdxl", num_steps=50, guidance=5.0, precision="bf16", sche
     cfg.use_graphs = 1 if graphs else 0
     cfg.scheduler = SCHEDULERS[scheduler]
     cfg.noise_seed = noise_seed
+    cfg.cfg_split = 1 if cfg_split else 0
     if weights is not None:
         cfg.weights = weights.ctypes.data_as(C.POINTER(C.c_float))
         cfg.weights_len = weights.size

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--scheme", default="pcpp")
     ap.add_argument("--same-gpu", action="store_true")
+    ap.add_argument("--cfg-split", action="store_true", help="CFG device split: world = 2 x patches")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
 
@@ -44,7 +45,8 @@ def main():
     dev = 0 if a.same_gpu else int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
     dist.init_process_group("gloo")
-    n = world
+    n = world // 2 if a.cfg_split else world
+    patch = rank % n
     blob = _data.blob(a.model)
     wts = inputs.round_to_bf16(blob) if a.precision == "bf16" else blob
     cond = _data.cond(a.model)
@@ -52,19 +54,19 @@ def main():
     h = a.H // n
 
     cfg = pcpp.make_config(model=a.model, num_steps=a.S, precision=a.precision, scheme=a.scheme,
-                           backend="peer", rank=rank, world=world)
+                           backend="peer", rank=rank, world=world, cfg_split=a.cfg_split)
     plan = pcpp.Plan(a.H, a.H, 4, n, a.p, a.w, cfg, wts)
     plan.pcpp_set_cond(cond)
     handles = [None] * world
     dist.all_gather_object(handles, plan.pcpp_peer_handle())
     plan.pcpp_peer_connect(handles)
-    lat = torch.from_numpy(np.ascontiguousarray(xT[rank * h:(rank + 1) * h])).cuda()
+    lat = torch.from_numpy(np.ascontiguousarray(xT[patch * h:(patch + 1) * h])).cuda()
     xs = []
     for k in range(a.steps):
         plan.pcpp_step(lat, k)
         torch.cuda.synchronize()
         xs.append(lat.cpu().numpy().copy())
-    x0 = plan.pcpp_sample(np.ascontiguousarray(xT[rank * h:(rank + 1) * h]), cond) if a.S <= 8 else None
+    x0 = plan.pcpp_sample(np.ascontiguousarray(xT[patch * h:(patch + 1) * h]), cond) if a.S <= 8 else None
     info = plan.pcpp_query()
     allx = [None] * world
     dist.all_gather_object(allx, (xs, x0))
@@ -72,7 +74,7 @@ def main():
 
     if rank == 0:
         cfg2 = pcpp.make_config(model=a.model, num_steps=a.S, precision=a.precision, scheme=a.scheme,
-                                backend="loopback")
+                                backend="loopback", cfg_split=a.cfg_split)
         lp = pcpp.Plan(a.H, a.H, 4, n, a.p, a.w, cfg2, wts)
         lp.pcpp_set_cond(cond)
         full = torch.from_numpy(xT.copy()).cuda()
@@ -85,9 +87,10 @@ def main():
         lp.close()
         steps = []
         for k in range(a.steps):
-            got = np.concatenate([allx[r][0][k] for r in range(world)], axis=0)
-            steps.append(int(np.sum(got != ref[k])))
-        res = {"case": vars(a), "mismatches_per_step": steps, "backend": info["backend"],
+            for br in range(world // n):          # every branch group holds the whole trajectory
+                got = np.concatenate([allx[br * n + r][0][k] for r in range(n)], axis=0)
+                steps.append(int(np.sum(got != ref[k])))
+        res = {"case": vars(a), "mismatches_per_step": steps, "backend": info["backend"], "bytes_eps": info["bytes_eps"],
                "bytes_counted_async": info["bytes_counted_async"],
                "finite": bool(all(np.isfinite(x).all() for x in ref))}
         if ref_x0 is not None:

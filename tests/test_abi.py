@@ -117,3 +117,27 @@ def test_arena_memory_plan(model, H, n, prec):
     assert 0 < info["arena_bytes_per_rank"] <= info["arena_bytes_unplanned"]
     if model == "sdxl":
         assert info["arena_bytes_per_rank"] < 0.75 * info["arena_bytes_unplanned"]
+
+
+@pytest.mark.parametrize("model,H,n,p", [("sdxl", 128, 4, 0.8), ("sdxl", 128, 2, 0.3), ("tiny", 32, 2, 0.25), ("sdxl", 128, 1, 0.0)])
+def test_cfg_split_plan_math(model, H, n, p):
+    # the CFG device split: per-branch exchanges within each group, 2 x the batch-1 bytes of one
+    # group = the batch-2 bytes of the same n; the eps swap moves one fp32 patch per rank and step
+    base = pcpp.pcpp_plan_info(H, H, 4, n, p, 1, pcpp.make_config(model=model))
+    sp = pcpp.pcpp_plan_info(H, H, 4, n, p, 1, pcpp.make_config(model=model, cfg_split=True))
+    assert sp["bytes_counted_async"] == sp["bytes_async"] == base["bytes_async"]
+    assert sp["bytes_counted_warmup"] == base["bytes_counted_warmup"]
+    assert sp["bytes_eps"] == 2 * n * (H // n) * H * 4 * 4
+    assert abs(sp["step_flops_rank_max"] * 2 - base["step_flops_rank_max"]) <= 1e-9 * base["step_flops_rank_max"]
+
+
+def test_cfg_split_validation():
+    C = pcpp.make_config
+    with pytest.raises(pcpp.PcppError):      # NCCL would need per-branch communicators
+        pcpp.pcpp_plan_info(128, 128, 4, 2, 0.3, 1, C(model="sdxl", cfg_split=True, backend="nccl", world=4, rank=0))
+    with pytest.raises(pcpp.PcppError):      # PEER world must be 2 n
+        pcpp.pcpp_plan_info(128, 128, 4, 2, 0.3, 1, C(model="sdxl", cfg_split=True, backend="peer", world=2, rank=0))
+    with pytest.raises(pcpp.PcppError):
+        pcpp.pcpp_plan_info(32, 32, 4, 2, 0.3, 1, C(model="tiny_xf", cfg_split=True))
+    assert pcpp.pcpp_plan_info(128, 128, 4, 2, 0.3, 1, C(model="sdxl", cfg_split=True, backend="peer", world=4,
+                                                         rank=3))["backend"] == pcpp.COMM_PEER

@@ -35,10 +35,10 @@ def oracle_run(model, H, n, p, w, S, precision, scheme, max_steps, scheduler="dd
 
 
 def lib_run(model, H, n, p, w, S, precision, scheme, max_steps, kernels="auto", graphs=True, scheduler="ddim",
-            noise_seed=0):
+            noise_seed=0, cfg_split=False):
     import torch
     cfg = pcpp.make_config(model=model, num_steps=S, precision=precision, scheme=scheme, kernels=kernels,
-                           graphs=graphs, scheduler=scheduler, noise_seed=noise_seed)
+                           graphs=graphs, scheduler=scheduler, noise_seed=noise_seed, cfg_split=cfg_split)
     plan = pcpp.Plan(H, H, 4, n, p, w, cfg, weights(model, precision))
     plan.pcpp_set_cond(_data.cond(model))
     lat = torch.from_numpy(np.array(_data.latent(H, H))).cuda()
@@ -274,3 +274,29 @@ def test_comm_off_debug_mode(cuda_ok):
     assert not np.array_equal(off[2], ref[2])            # async steps read older stale bands
     for k in range(4):
         assert np.array_equal(back[k], ref[k]), k
+
+
+# CFG device split (§2.2): 2 x n virtual ranks, branch b over the n patches as
+# batch 1, eps swapped between partners every step.  Same arithmetic as batch 2 per rank (reading
+# D27), so the oracle of the same (n, p) is the reference.
+SPLIT = [
+    ("tiny", 32, 1, 0.0, 0, 4, "fp32", "pcpp", 4),
+    ("tiny", 32, 2, 0.25, 1, 4, "fp32", "pcpp", 4),
+    ("tiny", 32, 4, 0.5, 1, 4, "bf16", "pcpp", 3),
+    ("tiny", 32, 2, 0.5, 1, 4, "fp32", "fullmap", 3),
+    ("sdxl", 32, 2, 0.3, 1, 50, "bf16", "pcpp", 3),
+    ("sdxl", 32, 4, 0.8, 1, 50, "bf16", "pcpp", 3),
+    ("sdxl", 32, 2, 0.3, 1, 50, "fp32", "pcpp", 2),
+]
+
+
+@pytest.mark.parametrize("case", SPLIT, ids=lambda c: "-".join(map(str, c)))
+def test_cfg_split_matches_oracle(cuda_ok, case):
+    ref = oracle_run(*case)
+    got, info = lib_run(*case, cfg_split=True)
+    errs = [rel_l2(g, r) for g, r in zip(got, ref)]
+    print(case, "cfg_split rel-L2 per step:", ["%.2e" % e for e in errs])
+    assert all(e <= TOL[case[6]] for e in errs), errs
+    n, H = case[2], case[1]
+    assert info["bytes_eps"] == 2 * n * (H // n) * H * 16
+    assert info["simt_fallbacks"] == 0

@@ -23,16 +23,29 @@ CASES = [
     ("sdxl", 32, 4, 0.8, 2, 50, 5, "bf16", "pcpp"),
 ]
 
+# CFG device split: 2 x n processes, branch groups of n patches + the per-step
+# eps swap between partners
+SPLIT = [
+    # model, H, n, p, w, S, steps, precision, scheme
+    ("tiny", 32, 1, 0.0, 1, 4, 4, "bf16", "pcpp"),
+    ("tiny", 32, 2, 0.25, 1, 4, 4, "fp32", "pcpp"),
+    ("sdxl", 32, 2, 0.3, 1, 50, 4, "bf16", "pcpp"),
+]
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c)))
-def test_peer_backend_multiprocess_bitwise_equals_loopback(cuda_ok, case, tmp_path):
+
+@pytest.mark.parametrize("split", [False, True], ids=["batch2", "cfgsplit"])
+@pytest.mark.parametrize("case", CASES + SPLIT, ids=lambda c: "-".join(map(str, c)))
+def test_peer_backend_multiprocess_bitwise_equals_loopback(cuda_ok, case, split, tmp_path):
     model, H, n, p, w, S, steps, prec, scheme = case
+    if split != (case in SPLIT):
+        pytest.skip("case list of the other mode")
     out = tmp_path / "res.json"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+    nproc = 2 * n if split else n
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + (os.getpid() % 400)}",
            os.path.join(ROOT, "tests", "_peer_worker.py"), "--same-gpu", "--model", model, "--H", str(H),
            "--p", str(p), "--w", str(w), "--S", str(S), "--steps", str(steps), "--precision", prec,
-           "--scheme", scheme, "--out", str(out)]
+           "--scheme", scheme, "--out", str(out)] + (["--cfg-split"] if split else [])
     # heuristic GEMM configurations: every process (ranks and the loopback reference) picks the same
     # split-K / tile choice, so the comparison can be bitwise (plan-time autotuning is timing-dependent)
     env = dict(os.environ, PYTHONPATH=ROOT, PCPP_AUTOTUNE="0")
@@ -42,3 +55,5 @@ def test_peer_backend_multiprocess_bitwise_equals_loopback(cuda_ok, case, tmp_pa
     print(res)
     assert res["backend"] == 2
     assert res["ok"], res
+    if split:
+        assert res["bytes_eps"] == 2 * n * (H // n) * H * 16

@@ -154,3 +154,30 @@ def test_P2_P6_xf(n, p):
         ef, _ = pcpp.forward_pair(pcpp.Config(model="tiny_xf", n=2, p=1.0), blob, xT, 751, c, "fresh", "fresh", ctxt)
         ref = torch_ref.eps("tiny_xf", blob, xT, 751, c, ctxt)
         np.testing.assert_allclose(np.concatenate(ef, axis=1), ref, atol=1e-11 * max(1.0, np.abs(ref).max()))
+
+
+def test_timestep_embedding_known_answer():
+    """Reading D19 pinned by a hand-derived vector: with lin1 selecting sinusoid entries 32 (cos) and
+    64 + 48 (sin) of the tiny model (half = 64, f_j = 10^(-4 j / 64)), lin2 = identity on those two
+    units and zero biases, tau = 1000 gives f_32 = 1/100, f_48 = 1/1000, so
+    emb = [silu(cos 10), silu(sin 1), 0, ...] for the uncond branch and emb + c for the cond one."""
+    import math
+    man = M.manifest("tiny")
+    blob = np.zeros(sum(int(np.prod(s)) for _, s, _ in man))
+    offs, off = {}, 0
+    for name, shape, _ in man:
+        offs[name] = (off, shape)
+        off += int(np.prod(shape))
+    o1, (T, S) = offs["time.lin1.w"]
+    blob[o1 + 0 * S + 32] = 1.0                 # hidden 0 <- sinusoid[32] = cos(tau f_32)
+    blob[o1 + 1 * S + 64 + 48] = 1.0            # hidden 1 <- sinusoid[64 + 48] = sin(tau f_48)
+    o2, _ = offs["time.lin2.w"]
+    blob[o2 + 0 * T + 0] = 1.0
+    blob[o2 + 1 * T + 1] = 1.0
+    c = np.zeros(T); c[5] = 2.5
+    emb = M.timestep_embedding(M.Params("tiny", blob), "tiny", 1000, c)
+    silu = lambda v: v / (1.0 + math.exp(-v))
+    want = np.zeros(T); want[0] = silu(math.cos(10.0)); want[1] = silu(math.sin(1.0))
+    np.testing.assert_allclose(emb[0], want, atol=1e-13)
+    want[5] = 2.5
+    np.testing.assert_allclose(emb[1], want, atol=1e-13)

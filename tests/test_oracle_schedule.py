@@ -185,3 +185,26 @@ def test_ancestral_reduces_to_eq3_eq4_on_full_ladder():
         np.testing.assert_allclose(mean, SCH.ddpm_mean(x, e, t), rtol=1e-9, atol=1e-9)
         sig = SCH.ancestral_coeffs(1000, k)[4]
         assert abs(sig ** 2 - (1 - ab[t - 1]) / (1 - ab[t]) * be[t]) <= 1e-12
+
+
+def test_box_muller_known_answer_invariants():
+    """Reading D24's z, pinned by invariants of the Box-Muller map rather than its formula: for each
+    word pair, z_a^2 + z_b^2 = -2 ln u1 and atan2(z_b, z_a) = 2 pi u2 (mod 2 pi), with u1, u2 the
+    documented 53-bit uniforms of numpy's independent Philox4x64 words.  A swapped cos / sin, a wrong
+    shift or a mis-paired word fails one of them."""
+    import math
+    from oracle.schedule import noise_token
+    for seed, k, g in ((0, 0, 0), (12, 3, 517), (2 ** 40 + 7, 49, 65535)):
+        # numpy's Philox increments its 256-bit counter before the first block: start one below (g, k, 0, 0)
+        c = (g + (k << 64) - 1) % (1 << 256)
+        bg = np.random.Philox(counter=np.array([(c >> (64 * i)) & (2 ** 64 - 1) for i in range(4)], dtype=np.uint64),
+                              key=np.array([seed, 0], dtype=np.uint64))
+        words = [int(v) for v in bg.random_raw(4)]
+        z = noise_token(seed, k, g)
+        for j in range(2):
+            u1 = ((words[2 * j] >> 11) + 0.5) * 2.0 ** -53
+            u2 = (words[2 * j + 1] >> 11) * 2.0 ** -53
+            za, zb = z[2 * j], z[2 * j + 1]
+            assert abs(za * za + zb * zb - (-2.0 * math.log(u1))) <= 1e-12 * max(1.0, -2.0 * math.log(u1))
+            ang = math.atan2(zb, za) % (2 * math.pi)
+            assert abs(ang - (2 * math.pi * u2) % (2 * math.pi)) <= 1e-9
