@@ -143,8 +143,9 @@ __global__ void __launch_bounds__(128) gn_finalize_kernel(const double* __restri
   }
 }
 
-void launch_gn_finalize(const double* part, int nslots, double* m_out, cudaStream_t s) {
-  launch_pdl(gn_finalize_kernel, dim3(2 * G), dim3(128), 0, s, part, nslots, m_out);
+// m_out holds [B][G][2] (B = the rank's CFG batch: 2, or 1 with the CFG device split)
+void launch_gn_finalize(const double* part, int nslots, int B, double* m_out, cudaStream_t s) {
+  launch_pdl(gn_finalize_kernel, dim3(B * G), dim3(128), 0, s, part, nslots, m_out);
 }
 
 // stats pass over x (+ x1 for a channel concat) and the finalize of its per-CTA slots
@@ -153,7 +154,7 @@ void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
   const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
   if (a.x0.dtype == DT_F32) launch_pdl(gn_stats_kernel<float>, dim3(a.nchunk), dim3(NT), smem, s, a);
   else launch_pdl(gn_stats_kernel<bf16>, dim3(a.nchunk), dim3(NT), smem, s, a);
-  launch_gn_finalize(a.partial, a.nchunk, a.m_out, s);
+  launch_gn_finalize(a.partial, a.nchunk, a.x0.B, a.m_out, s);
 }
 
 // ---- apply -------------------------------------------------------------------------------------

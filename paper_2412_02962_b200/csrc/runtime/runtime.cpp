@@ -874,7 +874,7 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           for (int vr = 0; vr < nr && do_op; ++vr) {
             const int slots = P.gn_slots[(size_t)vr * P.gns.size() + op.xid];
             if (slots > 0)
-              launch_gn_finalize(reinterpret_cast<const double*>(P.rm[vr].arena + P.off_epart), slots,
+              launch_gn_finalize(reinterpret_cast<const double*>(P.rm[vr].arena + P.off_epart), slots, P.B,
                                  reinterpret_cast<double*>(P.rm[vr].arena + gx.off_m[par]), s);
             else
               launch_gn_stats(stats_args(vr), s);
