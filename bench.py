@@ -195,6 +195,7 @@ def _progress(msg):
 
 
 TUNE_FILE = os.path.join(ROOT, "profiles", "gemm_tune_b200.txt")
+DIST_DEV = "cuda"          # device of the small tensors of the process-group collectives (cpu under gloo)
 
 
 def _comm_off_timing(plan, lat, pre, steps, ms, dist, torch):
@@ -223,7 +224,7 @@ def _comm_off_timing(plan, lat, pre, steps, ms, dist, torch):
             plan.pcpp_debug_comm_off(False)
         except Exception as e:
             err = err or repr(e)[:200]
-    t = torch.tensor([ms_off, 1.0 if err else 0.0], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms_off, 1.0 if err else 0.0], dtype=torch.float64, device=DIST_DEV)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)        # outside the try: every rank gets here
     if t[1].item() > 0:
         return {"error": err or "failed on another rank"}
@@ -300,11 +301,20 @@ def main():
         raise SystemExit(f"WORLD_SIZE={world} but --gpus {N}")
     if world == 1 and N > 1:
         raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
-    torch.cuda.set_device(local)
+    # PCPP_BENCH_ONE_GPU=1 (test mode): every rank on cuda:0 with a gloo process group -- exercises the
+    # N > 1 code path (PEER exchanges between processes, COMM_OFF, profiles, e2e) on a one-GPU box;
+    # its timings are of ranks sharing one GPU and mean nothing
+    one_gpu = os.environ.get("PCPP_BENCH_ONE_GPU") == "1"
+    dev = "cpu" if one_gpu else "cuda"
+    globals()["DIST_DEV"] = dev
+    torch.cuda.set_device(0 if one_gpu else local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     split = args.cfg_split and N > 1
     if split and N % 2:
         raise SystemExit("--cfg-split needs an even number of GPUs")
@@ -324,7 +334,7 @@ def main():
     def make_plan(backend):
         nccl_id = None
         if backend == "nccl":
-            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            idt = torch.zeros(128, dtype=torch.uint8, device=DIST_DEV)
             if rank == 0:
                 idt.copy_(torch.frombuffer(bytearray(pcpp.pcpp_get_unique_id()), dtype=torch.uint8))
             dist.broadcast(idt, 0)
@@ -345,7 +355,7 @@ def main():
     except Exception as e:        # e.g. CUDA IPC unavailable: every rank switches to NCCL together
         backend_note, ok = f"{backend} backend failed ({repr(e)[:160]})", 0.0
     if world > 1:
-        t = torch.tensor([ok], device="cuda")
+        t = torch.tensor([ok], device=DIST_DEV)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         ok = float(t.item())
     if ok < 1.0:
@@ -384,7 +394,7 @@ def main():
     _progress("timed steps done")
     ms = ev0.elapsed_time(ev1) / args.steps
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=DIST_DEV)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     info = plan.pcpp_query()
@@ -459,7 +469,7 @@ def main():
             dts.append(time.perf_counter() - t0)
         dt = sum(dts) / len(dts)
         if dist is not None:
-            t = torch.tensor([dt], device="cuda")
+            t = torch.tensor([dt], device=DIST_DEV)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": dt * 1000.0 / S, "unit": "ms/step", "sample_ms": dt * 1000.0, "num_steps": S,

@@ -10,6 +10,10 @@ namespace pcpp {
 
 bool pdl_enabled() { return true; }
 
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
 bool tc_available();
 bool gemm_tc_supported(const GemmArgs& g);
 bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s);

@@ -34,8 +34,11 @@ struct TcGemmParams {
   ActView res, out, out2;
   int splits, s_len;          // split-K: blockIdx.z covers k-steps [z*s_len, (z+1)*s_len)
   float* ws;                  // [splits][M][N] fp32 partials (M = tokens in layout order)
-  double* gn_part;            // fused GroupNorm statistics: [gridDim.x * 4 warps][B=2][G=32][2] fp64
+  double* gn_part;            // fused GroupNorm statistics: [gridDim.x CTAs][B=2][G=32][2] fp64
   int gn_cg;                  //   channels per group (N / 32)
+  double* gn_m;               //   non-null: the last CTA reduces the slots into gn_m[B][G][2]
+  unsigned* gn_ticket;        //   CTA arrival counter for that (zero between launches)
+  int gn_B;
 };
 
 // Extra shared memory of the stats-fused variant: per epilogue warp a 32 x 17-word bf16 transpose
@@ -259,6 +262,46 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
   }
 }
 
+// End of a stats-fused GEMM (epilogue warps 2-5 only, named barrier 1): the 4 warps' fp64 group
+// accumulators -> this CTA's slot (fixed order); with p.gn_m the last CTA to arrive sums every
+// CTA's slot in fixed order into gn_m (the consumer GroupNorm then needs no finalize launch).
+__device__ __forceinline__ void gn_cta_finish(const TcGemmParams& p, const double* st_acc) {
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const int t = threadIdx.x - 64;                      // 0..127 = (b, g, {sum, sumsq})
+  const double v = ((st_acc[t] + st_acc[128 + t]) + st_acc[256 + t]) + st_acc[384 + t];
+  p.gn_part[(size_t)blockIdx.x * 128 + t] = v;
+  if (!p.gn_m) return;
+  __shared__ unsigned last;
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (t == 0) last = atomicAdd(p.gn_ticket, 1u) == gridDim.x - 1 ? 1u : 0u;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (!last) return;
+  __threadfence();
+  // warp w sums slots k = w, w + 4, ... (lane = 4 consecutive entries, 8 loads in flight), then the 4
+  // warps' sums are combined in fixed order: a fixed summation order for a given grid size
+  const int w = t >> 5, l4 = (t & 31) * 4, nslot = gridDim.x;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int k0 = w; k0 < nslot; k0 += 32) {
+    double2 va[8], vb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + 4 * u;
+      const double2* q = reinterpret_cast<const double2*>(p.gn_part + (size_t)k * 128 + l4);
+      va[u] = k < nslot ? __ldcg(q) : make_double2(0.0, 0.0);
+      vb[u] = k < nslot ? __ldcg(q + 1) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { s0 += va[u].x; s1 += va[u].y; s2 += vb[u].x; s3 += vb[u].y; }
+  }
+  double* red = const_cast<double*>(st_acc);         // the warps' accumulators are consumed: reuse
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  red[w * 128 + l4] = s0; red[w * 128 + l4 + 1] = s1; red[w * 128 + l4 + 2] = s2; red[w * 128 + l4 + 3] = s3;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (t < p.gn_B * 64) p.gn_m[t] = (red[t] + red[128 + t]) + (red[256 + t] + red[384 + t]);
+  if (t == 0) *p.gn_ticket = 0u;                     // ready for the next launch (stream order)
+}
+
 template <int BN, bool ST>
 __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
@@ -398,10 +441,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
     }
-    if (ST) {
-      const double4 v = *reinterpret_cast<const double4*>(sacc + lane * 4);
-      *reinterpret_cast<double4*>(p.gn_part + ((size_t)blockIdx.x * 4 + q) * 128 + lane * 4) = v;
-    }
+    if (ST) gn_cta_finish(p, st_acc);
   }
   sm100::fence_before();
   __syncthreads();
@@ -645,10 +685,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
     }
-    if (ST) {
-      const double4 v = *reinterpret_cast<const double4*>(sacc + lane * 4);
-      *reinterpret_cast<double4*>(p.gn_part + ((size_t)blockIdx.x * 4 + q) * 128 + lane * 4) = v;
-    }
+    if (ST) gn_cta_finish(p, st_acc);
   }
   sm100::fence_before();
   sm100::cluster_sync();
@@ -669,6 +706,7 @@ static int launch_bn2(const TcGemmParams& p, cudaStream_t s) {   // returns the 
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at; cfg.numAttrs = 2;
+  count_launch();
   if (st) cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, true>, p);
   else cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, false>, p);
   return 2 * clusters;
@@ -786,12 +824,17 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   const int nsteps = p.taps * p.nkc;
   const long long M = (long long)g.rows_out * g.B * g.w_out;
   p.splits = 1; p.s_len = nsteps; p.ws = g.ws;
-  const bool st = gn_fusable(g);
-  if (st) { want_splits = 1; p.gn_part = g.gn_part; p.gn_cg = g.N / 32; }
   if (want_splits > 1 && g.ws && (size_t)want_splits * M * g.N <= g.ws_elems) {
     p.s_len = (nsteps + want_splits - 1) / want_splits;
     p.splits = (nsteps + p.s_len - 1) / p.s_len;
   }
+  // GroupNorm statistics ride on the epilogue of an unsplit GEMM; a split-K GEMM leaves them to the
+  // consumer GN's own statistics pass (gn_slots = 0)
+  const bool st = gn_fusable(g) && p.splits == 1;
+  if (st) {
+    p.gn_part = g.gn_part; p.gn_cg = g.N / 32; p.gn_B = g.B;
+    if (g.gn_m && g.gn_ticket) { p.gn_m = g.gn_m; p.gn_ticket = g.gn_ticket; }
+  } else if (g.gn_slots) *g.gn_slots = 0;
   if (pair) {
     // B box carries BN/2 rows per CTA
     if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN / 2)) return false;
@@ -801,7 +844,7 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
       case 160: grid = launch_bn2<160>(p, s); break;
       default: grid = launch_bn2<128>(p, s); break;
     }
-    if (st) *g.gn_slots = 4 * grid;
+    if (st) *g.gn_slots = p.gn_m ? -1 : grid;
   } else {
     int grid = 0;
     switch (BN) {
@@ -810,7 +853,7 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
       case 128: grid = launch_bn<128>(p, s); break;
       default: grid = launch_bn<64>(p, s); break;
     }
-    if (st) *g.gn_slots = 4 * grid;
+    if (st) *g.gn_slots = p.gn_m ? -1 : grid;
   }
   if (p.splits > 1) {
     const long long total = M * (g.N / 8);
@@ -905,10 +948,22 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
     if (!bn_ok(g, bn)) continue;
     if (pair && bn == 64) continue;
     for (int S = 1; S <= 6; ++S) {
-      if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems || gn_fusable(g) || g.geglu)) break;
+      if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems || g.geglu)) break;
+      // a split GEMM whose output feeds a GroupNorm pays that GN's statistics pass: timed with it
+      const bool stats_pass = S > 1 && gn_fusable(g);
+      GnStatsArgs sa;
+      if (stats_pass) {
+        sa.x0 = g.out; sa.c0 = g.out.C; sa.C = g.out.C;
+        sa.nchunk = gn_stats_chunks(g.out.rows, g.out.W);
+        sa.partial = reinterpret_cast<double*>(g.gn_part);
+        sa.m_out = reinterpret_cast<double*>(g.gn_part) + (size_t)sa.nchunk * 128;
+      }
       if (!launch_gemm_tc_cfg(g, s, bn, S, pair)) continue;      // warm
       cudaEventRecord(e0, s);
-      for (int r = 0; r < 3; ++r) launch_gemm_tc_cfg(g, s, bn, S, pair);
+      for (int r = 0; r < 3; ++r) {
+        launch_gemm_tc_cfg(g, s, bn, S, pair);
+        if (stats_pass) launch_gn_stats(sa, s);
+      }
       cudaEventRecord(e1, s);
       cudaEventSynchronize(e1);
       float ms = 0.f;

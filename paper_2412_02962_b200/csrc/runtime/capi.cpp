@@ -133,7 +133,8 @@ static void fill_info(Plan& P, pcpp_info* info) {
       default: nk += P.nr;
     }
   }
-  info->n_kernels_per_step = (int)nk;
+  // exact once a step has been enqueued (counted at the launches), else the static estimate
+  info->n_kernels_per_step = P.launches_per_step > 0 ? P.launches_per_step : (int)nk;
   double fl = 0, by = 0; int nl = 0;
   op_work(P, K_GEMM | K_ATTN, 0, &fl, &by, &nl);
   info->step_flops = fl;

@@ -149,6 +149,7 @@ pcpp_status plan_allocate(Plan& P) {
     }
   }
   P.off_epart = off; off = align256(off + (size_t)148 * 4 * 128 * sizeof(double));
+  P.off_tick = off; off = align256(off + std::max<size_t>(1, P.gns.size()) * sizeof(unsigned));
   P.gn_slots.assign((size_t)P.nr * P.gns.size(), 0);
   const size_t es = dtype_size(P.dtype);
   size_t gat_level[3] = {0, 0, 0};
@@ -760,8 +761,9 @@ pcpp_status context_setup(Plan& P, const float* ctx_host) {
 pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
   const int n = P.n, nr = P.nr;
   cudaStream_t s = P.s0;
+  const int lps_prev = P.launches_per_step;
   P.launches_per_step = 0;
-  const long long fb0 = simt_fallback_count();
+  const long long fb0 = simt_fallback_count(), lc0 = launch_count();
   // PEER: every peer has finished step k-1 (its compute and its pushes) before this step reads what
   // they pushed during k-1 and before this step pushes into the buffers they read during k-1
   if (P.backend == PCPP_COMM_PEER && P.world > 1 && (mask & K_XCH)) {
@@ -825,6 +827,8 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           if (op.gn_fuse >= 0) {
             g.gn_part = reinterpret_cast<double*>(P.rm[vr].arena + P.off_epart);
             g.gn_slots = &P.gn_slots[(size_t)vr * P.gns.size() + op.gn_fuse];
+            g.gn_m = reinterpret_cast<double*>(P.rm[vr].arena + P.gns[op.gn_fuse].off_m[par]);
+            g.gn_ticket = reinterpret_cast<unsigned*>(P.rm[vr].arena + P.off_tick) + op.gn_fuse;
           }
           if (op.geglu) {    // fused GEGLU epilogue on the tensor-core path, else GEMM into tmp + GEGLU kernel
             g.geglu = 1;
@@ -873,15 +877,17 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
         {
           for (int vr = 0; vr < nr && do_op; ++vr) {
             const int slots = P.gn_slots[(size_t)vr * P.gns.size() + op.xid];
+            if (slots < 0) continue;                 // the producer GEMM's last CTA wrote m[par]
             if (slots > 0)
               launch_gn_finalize(reinterpret_cast<const double*>(P.rm[vr].arena + P.off_epart), slots, P.B,
                                  reinterpret_cast<double*>(P.rm[vr].arena + gx.off_m[par]), s);
             else
               launch_gn_stats(stats_args(vr), s);
+            P.launches_per_step += slots > 0 ? 1 : 2;
           }
           if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
           for (int vr = 0; vr < nr && do_op; ++vr) launch_gn_apply(apply_args(vr), s);
-          P.launches_per_step += 2 * nr;
+          if (do_op) P.launches_per_step += nr;
         }
         break;
       }
@@ -977,6 +983,8 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
   }
   if (P.op_ev_on) cudaEventRecord(P.op_ev[P.ops.size()], s);
   P.simt_fallbacks = std::max<int>(P.simt_fallbacks, (int)(simt_fallback_count() - fb0));
+  // every kernel a whole step enqueued (exact); partial (profiling) steps leave the record alone
+  P.launches_per_step = mask == K_ALL ? (int)(launch_count() - lc0) : lps_prev;
   CK(cudaGetLastError());
   return PCPP_OK;
 }
