@@ -239,6 +239,14 @@ PCPP_API pcpp_status pcpp_profile(pcpp_plan_t plan, float* latent, int kind_mask
  * method's (stale data stays older than one step): timing only.  Drops cached step graphs; call
  * between steps.  PCPP_ERR_INVALID on a NULL plan. */
 PCPP_API pcpp_status pcpp_debug_comm_off(pcpp_plan_t plan, int on);
+
+/* GEMM timeline debug aid: with PCPP_GEMM_TRACE=1 in the environment, every 1-CTA tensor-core GEMM
+ * launch records %globaltimer stamps (ns) per CTA into a ring of 32 launches x 148 CTAs x 8 stamps
+ * {0 entry, 1 after griddepcontrol.wait, 2 first operand stage landed, 3 last MMA issued, 4 first
+ * accumulator ready, 5 epilogue done, 6 exit, 7 unused} (0 where a CTA did not run).  Copies the ring
+ * (32 * 148 * 8 u64) to HOST `out` (caller-owned, >= that size), clears it, and returns the number of launches
+ * recorded so far (the ring slot of launch i is i % 32), 0 if tracing is off, -1 on a CUDA error. */
+PCPP_API int pcpp_debug_gemm_trace(unsigned long long* out);
 PCPP_API void pcpp_destroy(pcpp_plan_t plan);
 PCPP_API const char* pcpp_last_error(void);
 

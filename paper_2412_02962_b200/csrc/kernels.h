@@ -36,9 +36,6 @@ struct GemmArgs {
   // gn_part [slots][B=2][G=32][2] fp64 and *gn_slots (host) receives the slot count, 0 if the
   // launch did not produce them (the consumer then runs the standalone stats kernel)
   double* gn_part = nullptr; int* gn_slots = nullptr;
-  // with gn_m / gn_ticket also set, the last CTA of the launch sums the slots itself (fixed order) into
-  // gn_m [B][G][2] and *gn_slots = -1 (no finalize launch); gn_ticket: a zeroed counter, reset after use
-  double* gn_m = nullptr; unsigned* gn_ticket = nullptr;
   // GEGLU epilogue (the _XF feed-forward, reading D25): D has N columns in 64-column blocks
   // [value 64 | gate 64] (the builder interleaves W_ff1's rows); out gets N / 2 columns
   // out[:, 64 k + j] = (D[:, 128 k + j] + bias) * gelu(D[:, 128 k + 64 + j] + bias)

@@ -34,11 +34,14 @@ struct TcGemmParams {
   ActView res, out, out2;
   int splits, s_len;          // split-K: blockIdx.z covers k-steps [z*s_len, (z+1)*s_len)
   float* ws;                  // [splits][M][N] fp32 partials (M = tokens in layout order)
+  unsigned long long* trace;  // debug (PCPP_GEMM_TRACE=1): per-CTA %globaltimer stamps [gridDim.x][8], else null
+  CUtensorMap mo, mo2;        // TMA-store maps of out / out2: box (32 ch, 32 w, 1, 1), SWIZZLE_64B
+  int csplit;                 // > 1: cluster split-K -- a cluster of csplit CTAs shares one tile, each a K
+                              //   range (splits == csplit); the partial tiles are summed through DSMEM
+  int tma_st;                 // 1: the epilogue stores through smem staging + TMA (bf16 out, Wbox >= 32)
   double* gn_part;            // fused GroupNorm statistics: [gridDim.x CTAs][B=2][G=32][2] fp64
   int gn_cg;                  //   channels per group (N / 32)
-  double* gn_m;               //   non-null: the last CTA reduces the slots into gn_m[B][G][2]
-  unsigned* gn_ticket;        //   CTA arrival counter for that (zero between launches)
-  int gn_B;
+
 };
 
 // Extra shared memory of the stats-fused variant: per epilogue warp a 32 x 17-word bf16 transpose
@@ -47,41 +50,51 @@ struct TcGemmParams {
 constexpr int ST_TILE_WORDS = 32 * 17;
 constexpr int ST_SMEM = 4 * ST_TILE_WORDS * 4 + 4 * 128 * 8;
 
+// Epilogue output staging: per epilogue warp one 32-row x 32-column bf16 tile (2 KB, SWIZZLE_64B
+// layout) that a TMA store writes out -- coalesced, asynchronous stores instead of one 64-byte
+// segment per thread and row (measured 2.6 us per 128 x 160 tile with row-per-thread stores).
+constexpr int STG_BYTES = 4 * 2048;
+// smem: [ring][barriers (1 KB)][staging 8 KB][ST: transpose tiles + accumulators]; <= 227 KB in all
+constexpr int SMEM_FIXED = 1024 /*align slack*/ + 1024 + STG_BYTES;
+constexpr int SMEM_MAX = 232448;
+
 template <int BN, bool ST = false>
 struct TcCfg {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int RING = 223232 - (ST ? ST_SMEM : 0);                      // <= 218 KB of smem in all
+  static constexpr int RING = SMEM_MAX - SMEM_FIXED - (ST ? ST_SMEM : 0);
   static constexpr int STAGES = (RING / STAGE) > 10 ? 10 : (RING / STAGE);
   static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;   // 2 accumulators
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + (ST ? ST_SMEM : 0);
+  static constexpr int SMEM = SMEM_FIXED + STAGES * STAGE + (ST ? ST_SMEM : 0);
 };
 
 // epilogue of one 128 x BN accumulator tile held in TMEM (this thread = one row): bias + temb +
-// residual -> bf16/fp32 store, or raw fp32 partials for split-K
-// bias + temb + residual for one row's 32-column chunk starting at column n0 + c
-__device__ __forceinline__ void epilogue_math(const TcGemmParams& p, float* f, int b, const uint4* rres, int n0, int c) {
-  if (p.bias) {                       // 16-byte vector loads (warp-uniform addresses: L1 broadcast)
-    const float4* bp = reinterpret_cast<const float4*>(p.bias + n0 + c);
+// residual -> bf16/fp32 store, or raw fp32 partials for split-K.
+// Per 32-column chunk the operands are prefetched one chunk ahead (EPI_PRE = 5 x 16 B registers):
+// pre[0..3] = this row's 32 residual bf16, pre[4] = {bias[col], temb[0][col], temb[1][col]} for the
+// lane's column col = n0 + c + lane -- broadcast by shuffles, so the chunk's critical path holds no
+// global load (the per-chunk bias / temb loads cost ~0.5 us per chunk of L2 latency).
+constexpr int EPI_PRE = 5;
+// must be called by all 32 lanes (shuffles); rows that are not valid compute garbage that is dropped
+__device__ __forceinline__ void epilogue_math(const TcGemmParams& p, float* f, int b, const uint4* pre, bool valid) {
+  if (p.bias) {
+    const float bl = __uint_as_float(pre[4].x);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float4 t = __ldg(bp + i);
-      f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
-    }
+    for (int i = 0; i < 32; ++i) f[i] += __shfl_sync(0xffffffffu, bl, i);
   }
   if (p.temb) {
-    const float4* tp = reinterpret_cast<const float4*>(p.temb + b * p.temb_ld + n0 + c);
+    const float t0 = __uint_as_float(pre[4].y), t1 = __uint_as_float(pre[4].z);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float4 t = __ldg(tp + i);
-      f[4 * i] += t.x; f[4 * i + 1] += t.y; f[4 * i + 2] += t.z; f[4 * i + 3] += t.w;
+    for (int i = 0; i < 32; ++i) {
+      const float a0 = __shfl_sync(0xffffffffu, t0, i), a1 = __shfl_sync(0xffffffffu, t1, i);
+      f[i] += b ? a1 : a0;
     }
   }
-  if (p.res.base) {                   // residual chunk, prefetched by the caller (rres = 32 bf16)
+  if (p.res.base && valid) {          // residual chunk, prefetched (32 bf16)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&rres[j]);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&pre[j]);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float2 t = __bfloat1622float2(h[i]);
@@ -90,13 +103,18 @@ __device__ __forceinline__ void epilogue_math(const TcGemmParams& p, float* f, i
     }
   }
 }
-// residual chunk [c, c+32) of this row (4 x 16 B); issued one chunk ahead of its use
-__device__ __forceinline__ void res_prefetch(const TcGemmParams& p, long long rrow, int c, bool valid, uint4* rres) {
+// chunk [c, c+32) operands of this row / lane, issued one chunk ahead of their use
+__device__ __forceinline__ void res_prefetch(const TcGemmParams& p, long long rrow, int n0, int c, bool valid, uint4* pre) {
   if (p.res.base && valid) {
     const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(p.res.base) + rrow + c);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) rres[j] = __ldg(rp + j);
+    for (int j = 0; j < 4; ++j) pre[j] = __ldg(rp + j);
   }
+  const int col = n0 + c + (threadIdx.x & 31);
+  const float bl = p.bias ? __ldg(p.bias + col) : 0.f;
+  const float t0 = p.temb ? __ldg(p.temb + col) : 0.f;
+  const float t1 = (p.temb && p.B > 1) ? __ldg(p.temb + p.temb_ld + col) : t0;
+  pre[4] = make_uint4(__float_as_uint(bl), __float_as_uint(t0), __float_as_uint(t1), 0u);
 }
 
 // Fused GroupNorm statistics of one 32-column chunk held by a warp (lane = row, u = the row's 32
@@ -147,21 +165,58 @@ __device__ __forceinline__ void gn_chunk_stats(uint32_t* stile, double* sacc, co
   __syncwarp();
 }
 
+// The same statistics read from the warp's SWIZZLE_64B staging tile (row rr = 64 B; 16-byte chunk j of
+// the row at chunk j ^ ((rr >> 1) & 3)): no extra transpose writes.
+__device__ __forceinline__ void gn_chunk_stats_stg(const uint8_t* stg, double* sacc, int b, unsigned bmask, int col0, int cg) {
+  const int lane = threadIdx.x & 31;
+  const int sh = (lane & 1) * 16, wj = lane >> 1;
+  const uint32_t* t32 = reinterpret_cast<const uint32_t*>(stg);
+  float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
+  const bool mixed = bmask != 0u && bmask != 0xffffffffu;
+#pragma unroll 8
+  for (int rr = 0; rr < 32; ++rr) {
+    const uint32_t wv = t32[rr * 16 + (((wj >> 2) ^ ((rr >> 1) & 3)) << 2) + (wj & 3)];
+    const float x = __uint_as_float((wv >> sh) << 16);
+    if (mixed && ((bmask >> rr) & 1u)) { s1 += x; q1 = fmaf(x, x, q1); } else { s0 += x; q0 = fmaf(x, x, q0); }
+  }
+  const int col = col0 + lane;
+  const int g = col / cg;
+  const int rem = cg - 1 - (col - g * cg);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const float t0 = __shfl_down_sync(0xffffffffu, s0, d), t1 = __shfl_down_sync(0xffffffffu, q0, d);
+    const float t2 = __shfl_down_sync(0xffffffffu, s1, d), t3 = __shfl_down_sync(0xffffffffu, q1, d);
+    if (d <= rem && lane + d < 32) { s0 += t0; q0 += t1; s1 += t2; q1 += t3; }
+  }
+  if (lane == 0 || rem == cg - 1) {
+    if (!mixed) {
+      double* a = sacc + (b * 32 + g) * 2;
+      a[0] += s0; a[1] += q0;
+    } else {
+      double* a = sacc + g * 2;
+      a[0] += s0; a[1] += q0; a[64] += s1; a[65] += q1;
+    }
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ long long res_row(const TcGemmParams& p, int r, int b, int w, int n0) {
   return p.res.base ? (((long long)r * p.res.B + b) * p.res.W + w) * p.res.C + n0 : 0;
 }
 
-// rres0: the residual of chunk 0, prefetched by the caller before it waited for the accumulator
+// rres0: chunk 0's epilogue operands, prefetched by the caller before it waited for the accumulator
 template <int BN, bool ST>
 __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t tacc, int r, int b, int w, bool valid,
                                               int n0, int z, uint32_t* stile, double* sacc, unsigned bmask,
-                                              const uint4* rres0) {
+                                              const uint4* rres0, uint8_t* stg) {
   const bool second = n0 >= p.n_split;
   const ActView& ov = second ? p.out2 : p.out;
   const int ncol0 = second ? n0 - p.n_split : n0;
   const long long orow = (((long long)r * ov.B + b) * ov.W + w) * ov.C + ncol0;
   const long long rrow = res_row(p, r, b, w, n0);
-  uint4 rcur[4] = {rres0[0], rres0[1], rres0[2], rres0[3]}, rnext[4];
+  uint4 rcur[EPI_PRE], rnext[EPI_PRE];
+#pragma unroll
+  for (int j = 0; j < EPI_PRE; ++j) rcur[j] = rres0[j];
   if (!ST && p.geglu) {
     // blocks of 128 accumulator columns = [value 64 | gate 64] -> 64 output columns (bf16)
     const long long grow = (((long long)r * p.out.B + b) * p.out.W + w) * p.out.C + n0 / 2;
@@ -210,21 +265,62 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
         *reinterpret_cast<float4*>(wp + c + 4 * j) = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
                                                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
     }
+  } else if (p.tma_st) {
+    // staged TMA-store epilogue: the warp's 32 rows x 32 columns -> swizzled smem -> one TMA store
+    const int lane = threadIdx.x & 31;
+    const int wq = __shfl_sync(0xffffffffu, w, 0), bq = __shfl_sync(0xffffffffu, b, 0), rq = __shfl_sync(0xffffffffu, r, 0);
+    const CUtensorMap* mo = second ? &p.mo2 : &p.mo;
+    uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 64);
+    const int sw = (lane >> 1) & 3;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      if (c + 32 < BN) res_prefetch(p, rrow, n0, c + 32, valid, rnext);
+      uint32_t v[32];
+      sm100::tmem_ld32(tacc + c, v);
+      sm100::tmem_wait_ld();
+      uint32_t uo[16];
+      {
+        float f[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+        epilogue_math(p, f, b, rcur, valid);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+          uo[i] = valid ? *reinterpret_cast<uint32_t*>(&h2) : 0u;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < EPI_PRE; ++j) rcur[j] = rnext[j];
+      if (lane == 0) sm100::bulk_wait_read<0>();     // the previous chunk's store has read the tile
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) rowp[j ^ sw] = make_uint4(uo[4 * j], uo[4 * j + 1], uo[4 * j + 2], uo[4 * j + 3]);
+      sm100::fence_proxy_async_smem();
+      __syncwarp();
+      if constexpr (ST) gn_chunk_stats_stg(stg, sacc, b, bmask, n0 + c, p.gn_cg);
+      // a warp whose first row lies past the tile's tokens (W < 128 without whole-row tiles) stores
+      // nothing: its box would land on the next row; otherwise rows past W are clipped by the TMA
+      if (lane == 0 && ((threadIdx.x >> 5) & 3) * 32 < p.Wbox * p.Bbox * p.Rbox) {   // warp q: rows 32 q ..
+        sm100::tma_store_4d(mo, stg, ncol0 + c, wq, bq, rq);
+        sm100::bulk_commit();
+      }
+    }
   } else {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
-      if (c + 32 < BN) res_prefetch(p, rrow, c + 32, valid, rnext);
+      if (c + 32 < BN) res_prefetch(p, rrow, n0, c + 32, valid, rnext);
       uint32_t v[32];
       sm100::tmem_ld32(tacc + c, v);
       sm100::tmem_wait_ld();
       if constexpr (ST) {
         // stats variant (bf16 out, no second output): every lane takes part in the warp transpose
         uint32_t uo[16];
-        if (valid) {
-          float f[32];
+        float f[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-          epilogue_math(p, f, b, rcur, n0, c);
+        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+        epilogue_math(p, f, b, rcur, valid);
+        if (valid) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
@@ -239,16 +335,16 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
         }
         gn_chunk_stats(stile, sacc, uo, b, bmask, n0 + c, p.gn_cg);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) rcur[j] = rnext[j];
+        for (int j = 0; j < EPI_PRE; ++j) rcur[j] = rnext[j];
         continue;
       }
-      if (!valid) continue;
       float f[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-      epilogue_math(p, f, b, rcur, n0, c);
+      epilogue_math(p, f, b, rcur, valid);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) rcur[j] = rnext[j];
+      for (int j = 0; j < EPI_PRE; ++j) rcur[j] = rnext[j];
+      if (!valid) continue;
       if (ov.dtype == DT_BF16) {
         bf16* po = reinterpret_cast<bf16*>(ov.base) + orow + c;
 #pragma unroll
@@ -262,49 +358,94 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
   }
 }
 
+__device__ __forceinline__ void trace_stamp(const TcGemmParams& p, int i) {
+  if (p.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * 8 + i] = t;
+  }
+}
+
 // End of a stats-fused GEMM (epilogue warps 2-5 only, named barrier 1): the 4 warps' fp64 group
-// accumulators -> this CTA's slot (fixed order); with p.gn_m the last CTA to arrive sums every
-// CTA's slot in fixed order into gn_m (the consumer GroupNorm then needs no finalize launch).
+// accumulators -> this CTA's slot, fixed order (gn_finalize then sums gridDim.x slots, not 4x as many).
+// Folding that finalize into the last CTA to arrive (fence + ticket + slot reduction) was measured
+// slower than the separate launch: +6 us per GEMM of tail against ~2 us for the PDL-launched finalize.
 __device__ __forceinline__ void gn_cta_finish(const TcGemmParams& p, const double* st_acc) {
   asm volatile("bar.sync 1, 128;" ::: "memory");
   const int t = threadIdx.x - 64;                      // 0..127 = (b, g, {sum, sumsq})
-  const double v = ((st_acc[t] + st_acc[128 + t]) + st_acc[256 + t]) + st_acc[384 + t];
-  p.gn_part[(size_t)blockIdx.x * 128 + t] = v;
-  if (!p.gn_m) return;
-  __shared__ unsigned last;
-  __threadfence();
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (t == 0) last = atomicAdd(p.gn_ticket, 1u) == gridDim.x - 1 ? 1u : 0u;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (!last) return;
-  __threadfence();
-  // warp w sums slots k = w, w + 4, ... (lane = 4 consecutive entries, 8 loads in flight), then the 4
-  // warps' sums are combined in fixed order: a fixed summation order for a given grid size
-  const int w = t >> 5, l4 = (t & 31) * 4, nslot = gridDim.x;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  for (int k0 = w; k0 < nslot; k0 += 32) {
-    double2 va[8], vb[8];
+  p.gn_part[(size_t)blockIdx.x * 128 + t] = ((st_acc[t] + st_acc[128 + t]) + st_acc[256 + t]) + st_acc[384 + t];
+}
+
+// Cluster split-K epilogue (epilogue warps): CTA z of the cluster owns rows [z R, (z + 1) R) of the
+// tile (R = 128 / csplit); warp q takes a 32-row block and every (4 / blocks)-th 32-column chunk, sums
+// the csplit partial tiles of its rows through DSMEM in cluster-rank order (fixed: deterministic),
+// then bias / temb / residual, the staged TMA store and the GroupNorm statistics as the plain path.
+template <int BN, bool ST, typename Decode>
+__device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_t* smem, uint8_t* stg_all, double* st_acc,
+                                                   const Decode& decode) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = warp & 3;
+  const int S = p.csplit, R = 128 / S, nrb = R / 32, wpr = 4 / nrb;
+  const int rb = q % nrb, cw = q / nrb;
+  const uint32_t z = sm100::cluster_rank();
+  int r0, b0, w0, n0, zz;
+  decode(blockIdx.x, r0, b0, w0, n0, zz);
+  const int m = (int)z * R + rb * 32 + lane;
+  const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
+  const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
+  const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
+  const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
+  double* sacc = st_acc + q * 128;
+  uint8_t* stg = stg_all + q * 2048;
+  const bool second = n0 >= p.n_split;
+  const int ncol0 = second ? n0 - p.n_split : n0;
+  const CUtensorMap* mo = second ? &p.mo2 : &p.mo;
+  const long long rrow = res_row(p, r, b, w, n0);
+  const int wq = __shfl_sync(0xffffffffu, w, 0), bq = __shfl_sync(0xffffffffu, b, 0), rq = __shfl_sync(0xffffffffu, r, 0);
+  const uint32_t row_addr = sm100::smem_u32(smem) + (uint32_t)(m * (BN + 4)) * 4u;
+  uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 64);
+  const int sw = (lane >> 1) & 3;
+  uint4 pre[EPI_PRE];
+#pragma unroll 1
+  for (int c = cw * 32; c < BN; c += wpr * 32) {
+    res_prefetch(p, rrow, n0, c, valid, pre);
+    float f[32];
+#pragma unroll 1
+    for (int k = 0; k < S; ++k) {
+      const uint32_t a = sm100::mapa(row_addr + (uint32_t)c * 4u, (uint32_t)k);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int k = k0 + 4 * u;
-      const double2* q = reinterpret_cast<const double2*>(p.gn_part + (size_t)k * 128 + l4);
-      va[u] = k < nslot ? __ldcg(q) : make_double2(0.0, 0.0);
-      vb[u] = k < nslot ? __ldcg(q + 1) : make_double2(0.0, 0.0);
+      for (int j = 0; j < 8; ++j) {
+        const float4 v = sm100::ld_dsmem_f4(a + 16u * j);
+        if (k == 0) { f[4 * j] = v.x; f[4 * j + 1] = v.y; f[4 * j + 2] = v.z; f[4 * j + 3] = v.w; }
+        else { f[4 * j] += v.x; f[4 * j + 1] += v.y; f[4 * j + 2] += v.z; f[4 * j + 3] += v.w; }
+      }
     }
+    epilogue_math(p, f, b, pre, valid);
+    uint32_t uo[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) { s0 += va[u].x; s1 += va[u].y; s2 += vb[u].x; s3 += vb[u].y; }
+    for (int i = 0; i < 16; ++i) {
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+      uo[i] = valid ? *reinterpret_cast<uint32_t*>(&h2) : 0u;
+    }
+    if (lane == 0) sm100::bulk_wait_read<0>();
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) rowp[j ^ sw] = make_uint4(uo[4 * j], uo[4 * j + 1], uo[4 * j + 2], uo[4 * j + 3]);
+    sm100::fence_proxy_async_smem();
+    __syncwarp();
+    if constexpr (ST) gn_chunk_stats_stg(stg, sacc, b, bmask, n0 + c, p.gn_cg);
+    if (lane == 0 && (int)z * R + rb * 32 < p.Wbox * p.Bbox * p.Rbox) {
+      sm100::tma_store_4d(mo, stg, ncol0 + c, wq, bq, rq);
+      sm100::bulk_commit();
+    }
   }
-  double* red = const_cast<double*>(st_acc);         // the warps' accumulators are consumed: reuse
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  red[w * 128 + l4] = s0; red[w * 128 + l4 + 1] = s1; red[w * 128 + l4 + 2] = s2; red[w * 128 + l4 + 3] = s3;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (t < p.gn_B * 64) p.gn_m[t] = (red[t] + red[128 + t]) + (red[256 + t] + red[384 + t]);
-  if (t == 0) *p.gn_ticket = 0u;                     // ready for the next launch (stream order)
+  if (lane == 0) sm100::bulk_wait<0>();
+  if (ST) gn_cta_finish(p, st_acc);
 }
 
 template <int BN, bool ST>
 __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
+  if (threadIdx.x == 0) trace_stamp(p, 0);
   // Persistent: CTA c handles work units c, c + gridDim.x, ...; a unit = (m tile, n tile, k split).
   // The smem ring (full/empty) runs continuously across units; two TMEM accumulators (tfull/tempty)
   // let the epilogue of unit i overlap the main loop of unit i+1.
@@ -320,7 +461,8 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   uint64_t* tfull = empty + Cfg::STAGES;     // [2]
   uint64_t* tempty = tfull + 2;              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint32_t* st_tile = reinterpret_cast<uint32_t*>(smem + Cfg::STAGES * Cfg::STAGE + 256);   // ST only
+  uint8_t* stg_all = smem + Cfg::STAGES * Cfg::STAGE + 1024;                                 // 4 x 2 KB staging
+  uint32_t* st_tile = reinterpret_cast<uint32_t*>(stg_all + STG_BYTES);                        // ST only
   double* st_acc = reinterpret_cast<double*>(st_tile + 4 * ST_TILE_WORDS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -336,15 +478,16 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   sm100::fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();                                   // inputs of this GEMM are produced by the previous kernel
+  if (threadIdx.x == 0) trace_stamp(p, 1);
 
   const int n_tiles = p.N / BN;
   const int units = p.m_tiles * n_tiles * p.splits;
   const int nsteps_all = p.taps * p.nkc;
   auto decode = [&](int u, int& r0, int& b0, int& w0, int& n0, int& z) {
-    const int mt = u % p.m_tiles;
-    const int rest = u / p.m_tiles;
+    int mt, rest;
+    if (p.csplit > 1) { z = u % p.csplit; const int t = u / p.csplit; mt = t % p.m_tiles; rest = t / p.m_tiles; }
+    else { mt = u % p.m_tiles; rest = u / p.m_tiles; z = rest / n_tiles; }
     n0 = (rest % n_tiles) * BN;
-    z = rest / n_tiles;
     if (p.rowtile) { r0 = mt * p.Rbox; b0 = 0; w0 = 0; }
     else { const int wt = mt % p.nWt; const int tb = mt / p.nWt; b0 = tb % p.B; r0 = tb / p.B; w0 = wt * p.Wbox; }
   };
@@ -398,6 +541,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
         for (int s = s_begin; s < s_end; ++s) {
           sm100::mbar_wait(&full[st], ph);
           sm100::fence_after();
+          if (tc == 0 && s == s_begin) trace_stamp(p, 2);
           const uint64_t ad = a_desc0 + (uint64_t)((st * Cfg::A_BYTES) >> 4);
           const uint64_t bd = b_desc0 + (uint64_t)((st * Cfg::B_BYTES) >> 4);
 #pragma unroll
@@ -410,6 +554,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
         }
         sm100::mma_commit(&tfull[a]);
       }
+      trace_stamp(p, 3);
     }
   } else {
     // epilogue: warp w reads TMEM lanes [32 (w%4), 32 (w%4) + 32)
@@ -424,27 +569,54 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       __syncwarp();
     }
     int tc = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tc) {
+    if (p.csplit > 1) {
+      // cluster split-K: this CTA's fp32 partial tile -> its smem (the ring is free: every MMA of this
+      // CTA has completed), rows padded to BN + 4 floats (conflict-free 16 B row accesses)
+      sm100::mbar_wait(&tfull[0], 0);
+      sm100::fence_after();
+      float* part = reinterpret_cast<float*>(smem);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        sm100::tmem_ld32(tmem + c + (uint32_t(q * 32) << 16), v);
+        sm100::tmem_wait_ld();
+        float4* dst = reinterpret_cast<float4*>(part + m * (BN + 4) + c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
+                               __uint_as_float(v[4 * j + 3]));
+      }
+    }
+    for (int u = blockIdx.x; p.csplit <= 1 && u < units; u += gridDim.x, ++tc) {
       int r0, b0, w0, n0, z;
       decode(u, r0, b0, w0, n0, z);
       const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
       const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
-      uint4 rres0[4];
-      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), 0, valid, rres0);   // overlaps the main loop
+      uint4 rres0[EPI_PRE];
+      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 0, valid, rres0);   // overlaps the main loop
       const int a = tc & 1;
       sm100::mbar_wait(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
+      if (tc == 0 && threadIdx.x == 64) trace_stamp(p, 4);
       const uint32_t tacc = tmem + a * BN + (uint32_t(q * 32) << 16);
-      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, stile, sacc, bmask, rres0);
+      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, stile, sacc, bmask, rres0, stg_all + q * 2048);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
     }
-    if (ST) gn_cta_finish(p, st_acc);
+    if (p.tma_st && lane == 0) sm100::bulk_wait<0>();   // staged stores complete before exit
+    if (threadIdx.x == 64) trace_stamp(p, 5);
+    if (ST && p.csplit <= 1) gn_cta_finish(p, st_acc);
+  }
+  if (p.csplit > 1) {
+    sm100::cluster_sync();                    // every CTA's partial tile is in its smem
+    if (warp >= 2) gemm_csplit_reduce<BN, ST>(p, smem, stg_all, st_acc, decode);
+    sm100::cluster_sync();                    // the peers' smem stays alive until every CTA has read it
   }
   sm100::fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_stamp(p, 6);
   if (warp == 1) sm100::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
 }
 
@@ -482,6 +654,17 @@ static bool encode_act(CUtensorMap* m, const ActView& v, int pad, int Wbox, int 
   cuuint32_t estr[4] = {1, (cuuint32_t)stride, 1, (cuuint32_t)stride};
   return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// TMA-store map of a bf16 output [rows][B][W][C] (row 0 at v.base; halo rows excluded, so the box
+// clipping also protects them): box (32 channels, 32 w, 1, 1), SWIZZLE_64B
+static bool encode_out(CUtensorMap* m, const ActView& v) {
+  cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.B, (cuuint64_t)v.rows};
+  cuuint64_t strides[3] = {(cuuint64_t)v.C * 2, (cuuint64_t)v.W * v.C * 2, (cuuint64_t)v.B * v.W * v.C * 2};
+  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v.base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 static bool encode_w(CUtensorMap* m, const void* w, int K, int N, int BN) {
@@ -524,6 +707,21 @@ bool gemm_tc_supported(const GemmArgs& g) {
 template <int BN>
 static int launch_bn(const TcGemmParams& p, cudaStream_t s) {   // returns the grid size
   const int units = p.m_tiles * (p.N / BN) * p.splits;
+  if (p.csplit > 1) {            // one unit per CTA, clusters of csplit CTAs along K
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units); cfg.blockDim = dim3(192); cfg.stream = s;
+    cfg.dynamicSmemBytes = p.gn_part ? TcCfg<BN, true>::SMEM : TcCfg<BN, false>::SMEM;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.csplit; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at; cfg.numAttrs = 2;
+    count_launch();
+    if (p.gn_part) cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, true>, p);
+    else cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, false>, p);
+    return units;
+  }
   const int grid = units < 148 ? units : 148;
   if (p.gn_part) launch_pdl(gemm_tc_kernel<BN, true>, dim3(grid), dim3(192), TcCfg<BN, true>::SMEM, s, p);
   else launch_pdl(gemm_tc_kernel<BN, false>, dim3(grid), dim3(192), TcCfg<BN, false>::SMEM, s, p);
@@ -542,10 +740,10 @@ struct TcCfg2 {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = (BN / 2) * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int RING = 223232 - (ST ? ST_SMEM : 0);
+  static constexpr int RING = SMEM_MAX - SMEM_FIXED - (ST ? ST_SMEM : 0);
   static constexpr int STAGES = (RING / STAGE) > 10 ? 10 : (RING / STAGE);
   static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + (ST ? ST_SMEM : 0);
+  static constexpr int SMEM = SMEM_FIXED + STAGES * STAGE + (ST ? ST_SMEM : 0);
 };
 
 // ST: the epilogue also accumulates the GroupNorm sums of the output (as the 1-CTA kernel); each
@@ -563,7 +761,8 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
   uint64_t* tfull = empty + Cfg::STAGES;     // [2]
   uint64_t* tempty = tfull + 2;              // [2] (leader's counts both CTAs' epilogue warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint32_t* st_tile = reinterpret_cast<uint32_t*>(smem + Cfg::STAGES * Cfg::STAGE + 256);   // ST only
+  uint8_t* stg_all = smem + Cfg::STAGES * Cfg::STAGE + 1024;                                 // 4 x 2 KB staging
+  uint32_t* st_tile = reinterpret_cast<uint32_t*>(stg_all + STG_BYTES);                        // ST only
   double* st_acc = reinterpret_cast<double*>(st_tile + 4 * ST_TILE_WORDS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -675,16 +874,18 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
       const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
       const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
-      uint4 rres0[4];
-      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), 0, valid, rres0);
+      uint4 rres0[EPI_PRE];
+      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 0, valid, rres0);
       const int a = tc & 1;
       sm100::mbar_wait_cluster(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
-      gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, stile, sacc, bmask, rres0);
+      gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, stile, sacc, bmask, rres0,
+                            stg_all + q * 2048);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
     }
+    if (p.tma_st && lane == 0) sm100::bulk_wait<0>();
     if (ST) gn_cta_finish(p, st_acc);
   }
   sm100::fence_before();
@@ -797,9 +998,31 @@ static bool bn_ok(const GemmArgs& g, int bn) {
   return true;
 }
 
+// debug timeline (PCPP_GEMM_TRACE=1, 1-CTA kernel): a ring of 32 launches x 148 CTAs x 8 stamps
+static unsigned long long* g_trace = nullptr;
+static int g_trace_next = 0;
+static unsigned long long* trace_slot() {
+  static const bool on = getenv("PCPP_GEMM_TRACE") && atoi(getenv("PCPP_GEMM_TRACE"));
+  if (!on) return nullptr;
+  if (!g_trace && cudaMalloc(&g_trace, (size_t)32 * 148 * 8 * 8) != cudaSuccess) return g_trace = nullptr;
+  return g_trace + (size_t)(g_trace_next++ % 32) * 148 * 8;
+}
+int gemm_trace_copy(unsigned long long* host, int max_launches) {
+  if (!g_trace) return 0;
+  const int n = max_launches < 32 ? max_launches : 32;
+  if (cudaMemcpy(host, g_trace, (size_t)n * 148 * 8 * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  if (cudaMemset(g_trace, 0, (size_t)32 * 148 * 8 * 8) != cudaSuccess) return -1;   // the next read sees fresh stamps only
+  return g_trace_next;
+}
+
+// pair: 0 = 1-CTA persistent kernel, 1 = 2-CTA (cta_group::2) pairs, 2 / 4 = cluster split-K over 2 / 4
+// CTAs (the 1-CTA kernel in clusters; want_splits is then ignored)
 static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int want_splits, int pair) {
   TcGemmParams p;
   memset(&p, 0, sizeof p);
+  const int csplit = pair >= 2 ? pair : 1;
+  if (pair >= 2) pair = 0;
+  if (!pair && csplit == 1) p.trace = trace_slot();
   // tile geometry: 128 output tokens = Wbox x Bbox x Rbox in (w, b, r) layout order
   // tile = 128 output tokens: a 128-wide row segment, or whole rows of every batch entry (W < 128)
   p.rowtile = g.w_out < 128 && 128 % (g.B * g.w_out) == 0;
@@ -824,17 +1047,26 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   const int nsteps = p.taps * p.nkc;
   const long long M = (long long)g.rows_out * g.B * g.w_out;
   p.splits = 1; p.s_len = nsteps; p.ws = g.ws;
-  if (want_splits > 1 && g.ws && (size_t)want_splits * M * g.N <= g.ws_elems) {
+  if (csplit > 1) {
+    if (g.geglu || nsteps < csplit) return false;
+    p.s_len = (nsteps + csplit - 1) / csplit;
+    if ((nsteps + p.s_len - 1) / p.s_len != csplit) return false;     // every CTA of the cluster has a K range
+    p.splits = csplit; p.csplit = csplit;
+  } else if (want_splits > 1 && g.ws && (size_t)want_splits * M * g.N <= g.ws_elems) {
     p.s_len = (nsteps + want_splits - 1) / want_splits;
     p.splits = (nsteps + p.s_len - 1) / p.s_len;
   }
+  // staged TMA-store epilogue: bf16 outputs whose warp row groups are 32 consecutive w of one (b, r)
+  if ((p.splits == 1 || p.csplit > 1) && !g.geglu && g.out.dtype == DT_BF16 && (!g.out2.base || g.out2.dtype == DT_BF16) &&
+      !(p.rowtile && p.Wbox % 32) && p.Wbox >= 32 && g.out.C % 8 == 0 && (!g.out2.base || g.out2.C % 8 == 0) &&
+      encode_out(&p.mo, g.out) && (!g.out2.base || encode_out(&p.mo2, g.out2)))
+    p.tma_st = 1;
   // GroupNorm statistics ride on the epilogue of an unsplit GEMM; a split-K GEMM leaves them to the
   // consumer GN's own statistics pass (gn_slots = 0)
-  const bool st = gn_fusable(g) && p.splits == 1;
-  if (st) {
-    p.gn_part = g.gn_part; p.gn_cg = g.N / 32; p.gn_B = g.B;
-    if (g.gn_m && g.gn_ticket) { p.gn_m = g.gn_m; p.gn_ticket = g.gn_ticket; }
-  } else if (g.gn_slots) *g.gn_slots = 0;
+  if (p.csplit > 1 && !p.tma_st) return false;      // the cluster reduction stores through the TMA path
+  const bool st = gn_fusable(g) && (p.splits == 1 || p.csplit > 1);
+  if (st) { p.gn_part = g.gn_part; p.gn_cg = g.N / 32; }
+  else if (g.gn_slots) *g.gn_slots = 0;
   if (pair) {
     // B box carries BN/2 rows per CTA
     if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN / 2)) return false;
@@ -844,7 +1076,7 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
       case 160: grid = launch_bn2<160>(p, s); break;
       default: grid = launch_bn2<128>(p, s); break;
     }
-    if (st) *g.gn_slots = p.gn_m ? -1 : grid;
+    if (st) *g.gn_slots = grid;
   } else {
     int grid = 0;
     switch (BN) {
@@ -853,9 +1085,9 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
       case 128: grid = launch_bn<128>(p, s); break;
       default: grid = launch_bn<64>(p, s); break;
     }
-    if (st) *g.gn_slots = p.gn_m ? -1 : grid;
+    if (st) *g.gn_slots = grid;
   }
-  if (p.splits > 1) {
+  if (p.splits > 1 && p.csplit <= 1) {
     const long long total = M * (g.N / 8);
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
@@ -890,8 +1122,9 @@ bool launch_gemm_tc(const GemmArgs& g, cudaStream_t s) {
   static const char* force = getenv("PCPP_GEMM_FORCE");
   if (force) {
     int bn = 0, sp = 1, pr = 0;
-    if (sscanf(force, "%d,%d,%d", &bn, &sp, &pr) >= 1 && bn_ok(g, bn) && !(pr && bn == 64))
-      return launch_gemm_tc_cfg(g, s, bn, sp, pr);
+    if (sscanf(force, "%d,%d,%d", &bn, &sp, &pr) >= 1 && bn_ok(g, bn) && !(pr == 1 && bn == 64) &&
+        launch_gemm_tc_cfg(g, s, bn, sp, pr))
+      return true;                   // a configuration illegal for this shape falls through to the tuned one
   }
   GemmChoice c;
   {
@@ -943,12 +1176,16 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
   GemmChoice best = heuristic(g);
   float best_ms = 1e30f;
   const int bns[4] = {256, 160, 128, 64};
-  for (int pair = 0; pair <= 1; ++pair)
+  const int m_tiles = g.w_out >= 128 ? g.rows_out * g.B * ((g.w_out + 127) / 128)
+                      : (128 % (g.B * g.w_out) == 0) ? (g.rows_out + 128 / (g.B * g.w_out) - 1) / (128 / (g.B * g.w_out))
+                      : g.rows_out * g.B;
+  for (int pair : {0, 1, 2, 4})
   for (int bn : bns) {
     if (!bn_ok(g, bn)) continue;
-    if (pair && bn == 64) continue;
+    if (pair == 1 && bn == 64) continue;
+    if (pair >= 2 && ((long long)m_tiles * (g.N / bn) * pair > 296 || nsteps < 2 * pair)) continue;   // cluster split-K: small grids only
     for (int S = 1; S <= 6; ++S) {
-      if (S > 1 && (!g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems || g.geglu)) break;
+      if (S > 1 && (pair >= 2 || !g.ws || nsteps / S < 4 || (size_t)S * M * g.N > g.ws_elems || g.geglu)) break;
       // a split GEMM whose output feeds a GroupNorm pays that GN's statistics pass: timed with it
       const bool stats_pass = S > 1 && gn_fusable(g);
       GnStatsArgs sa;

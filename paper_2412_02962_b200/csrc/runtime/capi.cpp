@@ -11,6 +11,7 @@
 #include "nccl_api.h"
 
 namespace pcpp {
+int gemm_trace_copy(unsigned long long* host, int max_launches);
 const char* last_error_msg();
 XGroup make_group_public(const Plan& P, const Op& op, int sync, int par, std::vector<Xfer>& lb);
 void launch_gemm_auto(const GemmArgs& g, bool allow_tc, cudaStream_t s);
@@ -438,6 +439,11 @@ pcpp_status pcpp_profile(pcpp_plan_t h, float* latent, int kind, int sync, int i
   op_work(P, (unsigned)kind, sync, &out->flops, &out->bytes, &out->launches);
   return PCPP_OK;
   GUARD_END
+}
+
+int pcpp_debug_gemm_trace(unsigned long long* out) {
+  if (!out) return -1;
+  return gemm_trace_copy(out, 32);
 }
 
 pcpp_status pcpp_debug_comm_off(pcpp_plan_t h, int on) {

@@ -149,7 +149,6 @@ pcpp_status plan_allocate(Plan& P) {
     }
   }
   P.off_epart = off; off = align256(off + (size_t)148 * 4 * 128 * sizeof(double));
-  P.off_tick = off; off = align256(off + std::max<size_t>(1, P.gns.size()) * sizeof(unsigned));
   P.gn_slots.assign((size_t)P.nr * P.gns.size(), 0);
   const size_t es = dtype_size(P.dtype);
   size_t gat_level[3] = {0, 0, 0};
@@ -827,8 +826,6 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           if (op.gn_fuse >= 0) {
             g.gn_part = reinterpret_cast<double*>(P.rm[vr].arena + P.off_epart);
             g.gn_slots = &P.gn_slots[(size_t)vr * P.gns.size() + op.gn_fuse];
-            g.gn_m = reinterpret_cast<double*>(P.rm[vr].arena + P.gns[op.gn_fuse].off_m[par]);
-            g.gn_ticket = reinterpret_cast<unsigned*>(P.rm[vr].arena + P.off_tick) + op.gn_fuse;
           }
           if (op.geglu) {    // fused GEGLU epilogue on the tensor-core path, else GEMM into tmp + GEGLU kernel
             g.geglu = 1;
@@ -877,7 +874,6 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
         {
           for (int vr = 0; vr < nr && do_op; ++vr) {
             const int slots = P.gn_slots[(size_t)vr * P.gns.size() + op.xid];
-            if (slots < 0) continue;                 // the producer GEMM's last CTA wrote m[par]
             if (slots > 0)
               launch_gn_finalize(reinterpret_cast<const double*>(P.rm[vr].arena + P.off_epart), slots, P.B,
                                  reinterpret_cast<double*>(P.rm[vr].arena + gx.off_m[par]), s);

@@ -128,8 +128,7 @@ struct Plan {
   // per-rank memory
   size_t rank_bytes = 0;
   size_t off_epart = 0;                 // per-rank GEMM-fused GN statistics partials
-  size_t off_tick = 0;                  // per-rank, per-GN arrival counters of the stats-fused GEMMs
-  std::vector<int> gn_slots;            // [nr][ngn]: slots the producer GEMM wrote (0: not fused, -1: finalized by it)
+  std::vector<int> gn_slots;            // [nr][ngn]: slots the producer GEMM wrote (0: not fused)
   std::vector<RankMem> rm;
   // global memory
   void* wmat = nullptr;  float* wf32 = nullptr;

@@ -71,7 +71,7 @@ SYMBOLS = ["pcpp_plan_schedule", "pcpp_profile", "pcpp_config_default", "pcpp_ge
            "pcpp_manifest_entry", "pcpp_plan", "pcpp_plan_info", "pcpp_set_cond", "pcpp_step",
            "pcpp_sample", "pcpp_reset", "pcpp_query", "pcpp_debug_comm_off", "pcpp_destroy", "pcpp_last_error",
            "pcpp_op_conv", "pcpp_op_attention", "pcpp_op_groupnorm", "pcpp_op_pack_rows",
-           "pcpp_op_cfg_ddim", "pcpp_peer_handle", "pcpp_peer_connect", "pcpp_set_context"]
+           "pcpp_op_cfg_ddim", "pcpp_peer_handle", "pcpp_peer_connect", "pcpp_set_context", "pcpp_debug_gemm_trace"]
 
 _lib = None
 
@@ -111,6 +111,7 @@ def lib():
     L.pcpp_plan_schedule.restype = I
     L.pcpp_profile.argtypes = [P, V, I, I, I, C.POINTER(pcpp_prof)]; L.pcpp_profile.restype = I
     L.pcpp_debug_comm_off.argtypes = [P, I]; L.pcpp_debug_comm_off.restype = I
+    L.pcpp_debug_gemm_trace.argtypes = [P]; L.pcpp_debug_gemm_trace.restype = I
     L.pcpp_last_error.argtypes = []; L.pcpp_last_error.restype = C.c_char_p
     L.pcpp_op_conv.argtypes = [V, I, I, I, I, I, I, V, V, V, V, V, I, I, I, V]; L.pcpp_op_conv.restype = I
     L.pcpp_op_attention.argtypes = [V, C.POINTER(C.c_void_p), C.POINTER(C.c_int), I, I, I, I, I, V, I, I, V]
@@ -324,3 +325,11 @@ def pcpp_op_pack_rows(src, row_bytes, r0, nrows, dst, stream=None):
 def pcpp_op_cfg_ddim(eps, latent, h, W, guidance, num_steps, k, stream=None):
     _chk(lib().pcpp_op_cfg_ddim(_ptr(eps), _ptr(latent), h, W, float(guidance), num_steps, k, stream),
          "pcpp_op_cfg_ddim")
+
+
+def pcpp_debug_gemm_trace():
+    """GEMM timeline ring (PCPP_GEMM_TRACE=1): returns (launches recorded, uint64 array [32][148][8])."""
+    import numpy as np
+    buf = np.zeros(32 * 148 * 8, dtype=np.uint64)
+    n = lib().pcpp_debug_gemm_trace(buf.ctypes.data)
+    return n, buf.reshape(32, 148, 8)

@@ -142,10 +142,12 @@ def test_sample_e2e_host_buffers(cuda_ok):
     assert rel_l2(x0, oracle_run(*case)[-1]) <= TOL["bf16"]
 
 
-@pytest.mark.parametrize("force", ["160,1,1", "128,1,1", "256,1,1", "160,1,0", "64,1,0", "128,3,0"])
+@pytest.mark.parametrize("force", ["160,1,1", "128,1,1", "256,1,1", "160,1,0", "64,1,0", "128,3,0", "160,1,2", "128,1,4",
+                                   "64,1,4"])
 def test_forced_gemm_configs(cuda_ok, force, tmp_path):
-    """Every tcgen05 GEMM variant the autotuner can pick (1-CTA / 2-CTA pair, BN, split-K, with and
-    without the fused GroupNorm statistics) reproduces the oracle on the SDXL-shaped stack."""
+    """Every tcgen05 GEMM variant the autotuner can pick (1-CTA / 2-CTA pair, BN, split-K through the
+    fp32 workspace, cluster split-K through DSMEM (pair = 2 / 4), with and without the fused GroupNorm
+    statistics) reproduces the oracle on the SDXL-shaped stack."""
     import os
     import subprocess
     import sys
