@@ -28,8 +28,15 @@ pl.pcpp_set_cond(inputs.make_cond(1280 if model.startswith("sdxl") else 512))
 if model.endswith("_xf"):
     pl.pcpp_set_context(inputs.make_context(77, 2048 if model.startswith("sdxl") else 256))
 lat = torch.from_numpy(np.ascontiguousarray(inputs.make_latent(res, res))).cuda()
+# PROF_RANGE=1: only the last step inside cudaProfilerStart/Stop (ncu --profile-from-start off)
+rng = os.environ.get("PROF_RANGE") == "1"
 for k in range(w + steps):
+    if rng and k == w + steps - 1:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
     pl.pcpp_step(lat, k)
 torch.cuda.synchronize()
+if rng:
+    torch.cuda.cudart().cudaProfilerStop()
 print("launches/step", pl.pcpp_query()["n_kernels_per_step"])
 pl.close()
