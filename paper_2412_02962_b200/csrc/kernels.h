@@ -73,7 +73,7 @@ void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s);
 // m_out[b][g][k] = sum over slots of part[slot][b][g][k] (fp64, fixed order): the finalize of the
 // GEMM-epilogue-fused statistics
 void launch_gn_finalize(const double* part, int nslots, int B, double* m_out, cudaStream_t s);
-int gn_stats_chunks(int rows, int W);
+int gn_stats_chunks(int rows, int W, int C);
 void gn_init();
 
 // mode 0: M = m_fresh (n = 1)

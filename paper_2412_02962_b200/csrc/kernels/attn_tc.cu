@@ -23,6 +23,7 @@ namespace pcpp {
 
 struct TcAttnParams {
   CUtensorMap mq, mkv[3];
+  CUtensorMap mo;             // the output [h][B][W][C] with Q's box: O leaves through smem + one TMA store
   int nsrc, rows[3];
   int nkeys[3];               // keys attended per source (token order r * W + w); rows * W unless masked
   int h, W, B, C;
@@ -337,6 +338,25 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
             *reinterpret_cast<float2*>(wp + 4 * u + 2) = make_float2(acc[4 * u + 2], acc[4 * u + 3]);
           *reinterpret_cast<float2*>(wp + 64) = make_float2(m, l);
         }
+      } else if constexpr (NWG == 1) {
+        // O (bf16) -> the Q tile's smem (free: every S MMA has completed), SW128 rows of 128 B, then
+        // one TMA store of the tile with Q's box (rows past h / W are clipped by the TMA)
+        const float inv = 1.f / l;
+        uint8_t* Qs = smem + SM_Q;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float t8[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t8[i] = acc[8 * u + i] * inv;
+          store8(reinterpret_cast<bf16*>(Qs + row * 128 + ((u ^ (row & 7)) << 4)), t8);
+        }
+        sm100::fence_proxy_async_smem();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (row == 0) {
+          sm100::tma_store_4d(&p.mo, Qs, head * 64, (qt % p.nWt) * p.Wbox, b, (qt / p.nWt) * p.Rbox);
+          sm100::bulk_commit();
+          sm100::bulk_wait<0>();
+        }
       } else if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
         const float inv = 1.f / l;
 #pragma unroll
@@ -389,6 +409,7 @@ bool launch_attn_tc(const AttnArgs& a, cudaStream_t s) {
   p.nWt = (a.W + p.Wbox - 1) / p.Wbox;
   p.box_bytes = 128u * p.Wbox * p.Rbox;
   if (!encode_tok(&p.mq, a.q, a.h, a.B, a.W, a.C, p.Wbox, p.Rbox)) return false;
+  if (!encode_tok(&p.mo, a.out, a.h, a.B, a.W, a.C, p.Wbox, p.Rbox)) return false;
   p.nsrc = 0;
   p.ntiles = 0;
   for (int i = 0; i < a.nsrc; ++i) {

@@ -1191,7 +1191,7 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
       GnStatsArgs sa;
       if (stats_pass) {
         sa.x0 = g.out; sa.c0 = g.out.C; sa.C = g.out.C;
-        sa.nchunk = gn_stats_chunks(g.out.rows, g.out.W);
+        sa.nchunk = gn_stats_chunks(g.out.rows, g.out.W, g.out.C);
         sa.partial = reinterpret_cast<double*>(g.gn_part);
         sa.m_out = reinterpret_cast<double*>(g.gn_part) + (size_t)sa.nchunk * 128;
       }

@@ -29,9 +29,11 @@ __host__ __device__ __forceinline__ Lanes lanes_for(int C) {
 }
 }  // namespace
 
-int gn_stats_chunks(int rows, int W) {   // CTAs of gn_stats: >= 64 tokens each, at most one wave
-  long long tok = (long long)rows * 2 * W;
-  long long c = tok / 64;
+// CTAs of gn_stats: at most one wave, and >= 2 tokens per token lane (wide C leaves few token lanes per
+// CTA: C = 2560 has one, so a fixed 64 tokens per CTA starved the kernel at 32 CTAs -- 54 us for 10 MB)
+int gn_stats_chunks(int rows, int W, int C) {
+  const long long tok = (long long)rows * 2 * W;
+  long long c = tok / (2 * lanes_for(C).ntl);
   if (c < 1) c = 1;
   if (c > 148) c = 148;
   return (int)c;
@@ -73,10 +75,11 @@ __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
     const int cc = second ? c - a.c0 : c;
     long long Tt = T0 + tl;
     int w = (int)(Tt % W), bq = (int)((Tt / W) % B);
-    for (; Tt < T1; Tt += 4LL * L.ntl) {
-      float x[4][8];
+    constexpr int U = sizeof(T) == 2 ? 8 : 4;      // 16-byte loads in flight per thread
+    for (; Tt < T1; Tt += (long long)U * L.ntl) {
+      float x[U][8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < U; ++k) {
         const long long Tk = Tt + (long long)k * L.ntl;
         if (Tk < T1) load8(vptr<T>(src, Tk, cc), x[k]);
         else {
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < U; ++k) {
         if (bq == 0) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) { s[0][e] += x[k][e]; q[0][e] = fmaf(x[k][e], x[k][e], q[0][e]); }

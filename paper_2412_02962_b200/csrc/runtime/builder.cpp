@@ -120,7 +120,7 @@ struct Builder {
     const TDesc& a = P.td[x0];
     int C = a.C + (x1 >= 0 ? P.td[x1].C : 0);
     GnX g{}; g.C = C; g.rows = a.rows; g.W = a.W;
-    g.nchunk = gn_stats_chunks(a.rows, a.W);
+    g.nchunk = gn_stats_chunks(a.rows, a.W, C);
     g.count = (double)(a.rows * P.n) * a.W * (C / GN_G);
     P.gns.push_back(g);
     Op& o = op(OP_GN); o.in0 = x0; o.in1 = x1; o.out = out; o.silu = silu;

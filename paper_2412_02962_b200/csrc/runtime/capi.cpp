@@ -556,7 +556,7 @@ pcpp_status pcpp_op_groupnorm(const void* x, int rows, int B, int W, int C, cons
   const int dt = dtype == PCPP_FP32 ? DT_F32 : DT_BF16;
   GnStatsArgs a;
   a.x0.base = const_cast<void*>(x); a.x0.rows = rows; a.x0.B = B; a.x0.W = W; a.x0.C = C; a.x0.dtype = dt;
-  a.c0 = C; a.C = C; a.nchunk = gn_stats_chunks(rows, W);
+  a.c0 = C; a.C = C; a.nchunk = gn_stats_chunks(rows, W, C);
   char* sc = reinterpret_cast<char*>(op_scratch(WS_GN, (size_t)a.nchunk * 128 * 8, true));
   if (!sc) { set_error("scratch alloc"); return PCPP_ERR_OOM; }
   a.partial = reinterpret_cast<double*>(sc);
