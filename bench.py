@@ -263,6 +263,7 @@ def loopback_line(pcpp, torch, np, inputs, res, nv, pv, scheme, S, cond, kernels
     for k in range(wv + 2):
         pl.pcpp_step(lat, k)
     t = time_steps(pl, lat, wv + 2, 5, torch)
+    info = pl.pcpp_query()                    # launches of an async step (before any COMM_OFF re-timing)
     t_off = None
     if comm_off and nv > 1 and scheme == "pcpp":        # the same steps with the exchange copies skipped
         pl.pcpp_debug_comm_off(True)
@@ -271,11 +272,11 @@ def loopback_line(pcpp, torch, np, inputs, res, nv, pv, scheme, S, cond, kernels
             pl.pcpp_step(lat, k)
         t_off = round(time_steps(pl, lat, wv + 2, 5, torch), 4)
         pl.pcpp_debug_comm_off(False)
-    info = pl.pcpp_query()
     pl.close()
     return {"scheme": scheme + ("+cfg_split" if split else ""), "n_patches": nv, "gpus": ranks, "p": pv,
             "ms_per_step_all_ranks": round(t, 4), "ms_per_rank": round(t / ranks, 4),
             "ms_per_step_all_ranks_comm_off": t_off, "step_flops_rank_max": info["step_flops_rank_max"],
+            "launches_per_step_all_ranks": info["n_kernels_per_step"],
             "bytes_exchanged_per_step": sum(info["bytes_counted_async"]) + info["bytes_eps"],
             "bytes_by_class": dict(zip(("attn", "conv", "gn", "eps"), info["bytes_counted_async"] + [info["bytes_eps"]]))}
 

@@ -69,7 +69,7 @@ struct GnStatsArgs {
   double* m_out = nullptr;       // [B][G][2]
   int nchunk = 0;
 };
-void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s);
+void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s, bool finalize = true);   // finalize: m_out from the slots
 // m_out[b][g][k] = sum over slots of part[slot][b][g][k] (fp64, fixed order): the finalize of the
 // GEMM-epilogue-fused statistics
 void launch_gn_finalize(const double* part, int nslots, int B, double* m_out, cudaStream_t s);
@@ -86,6 +86,9 @@ struct GnApplyArgs {
   int mode = 0; int nranks = 1;
   const double* m_fresh = nullptr; const double* m_prev = nullptr; const double* mall = nullptr;
   double count = 0;              // N = H_l W_l C/G (global)
+  // nslots > 0: m_fresh is not read but summed here from the producer's per-CTA partial slots
+  // part[slot][B=2][G][2] (fixed order; no finalize launch), and CTA 0 writes it to m_write
+  const double* part = nullptr; int nslots = 0; double* m_write = nullptr;
 };
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s);
 

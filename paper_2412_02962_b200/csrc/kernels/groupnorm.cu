@@ -152,27 +152,56 @@ void launch_gn_finalize(const double* part, int nslots, int B, double* m_out, cu
 }
 
 // stats pass over x (+ x1 for a channel concat) and the finalize of its per-CTA slots
-void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s) {
+void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s, bool finalize) {
   const Lanes L = lanes_for(a.C);
   const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
   if (a.x0.dtype == DT_F32) launch_pdl(gn_stats_kernel<float>, dim3(a.nchunk), dim3(NT), smem, s, a);
   else launch_pdl(gn_stats_kernel<bf16>, dim3(a.nchunk), dim3(NT), smem, s, a);
-  launch_gn_finalize(a.partial, a.nchunk, a.x0.B, a.m_out, s);
+  if (finalize) launch_gn_finalize(a.partial, a.nchunk, a.x0.B, a.m_out, s);
 }
 
 // ---- apply -------------------------------------------------------------------------------------
+// the fresh local sums m[b][g][k] from the producer's slots (nslots <= GN_MERGE_MAX_SLOTS = 48): 4
+// threads per entry, each summing every 4th slot in order, then the 4 in fixed order (deterministic);
+// CTA 0 publishes them to m_write
+__device__ __forceinline__ void gn_slots_sum(const GnApplyArgs& a, double* mf) {
+  __shared__ double red[4][128];
+  const int e = threadIdx.x & 127, q = threadIdx.x >> 7;     // NT = 512: q in [0, 4)
+  // every load of the thread in flight at once (nslots <= 48: at most 12), then summed in slot order
+  double v[12];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    const int k = q + 4 * i;
+    v[i] = k < a.nslots ? __ldcg(a.part + (size_t)k * 128 + e) : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 12; ++i) acc += v[i];
+  red[q][e] = acc;
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    const double v = (red[0][e] + red[1][e]) + (red[2][e] + red[3][e]);
+    mf[e] = v;
+    if (blockIdx.x == 0 && e < a.x0.B * 2 * G) a.m_write[e] = v;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void gn_prep(const GnApplyArgs& a, float* mu_s, float* rs_s) {
   const int B = a.x0.B;
+  __shared__ double mf_s[128];
+  if (a.nslots > 0) gn_slots_sum(a, mf_s);
+  const double* mf = a.nslots > 0 ? mf_s : a.m_fresh;
   for (int i = threadIdx.x; i < B * G; i += NT) {
     double M1, M2;
     if (a.mode == 0) {
-      M1 = a.m_fresh[2 * i]; M2 = a.m_fresh[2 * i + 1];
+      M1 = mf[2 * i]; M2 = mf[2 * i + 1];
     } else {
       M1 = 0.0; M2 = 0.0;
       for (int j = 0; j < a.nranks; ++j) { M1 += a.mall[(j * B * G + i) * 2]; M2 += a.mall[(j * B * G + i) * 2 + 1]; }
       if (a.mode == 2) {
-        M1 = M1 - a.m_prev[2 * i] + a.m_fresh[2 * i];
-        M2 = M2 - a.m_prev[2 * i + 1] + a.m_fresh[2 * i + 1];
+        M1 = M1 - a.m_prev[2 * i] + mf[2 * i];
+        M2 = M2 - a.m_prev[2 * i + 1] + mf[2 * i + 1];
       }
     }
     const double mu = M1 / a.count;
@@ -194,12 +223,28 @@ __global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a,
   pdl_wait();
   __shared__ float mu_s[2 * G], rs_s[2 * G];
   const int B = a.x0.B, C = a.C, cg = C / G, nv = C / 8, W = a.x0.W;
-  gn_prep(a, mu_s, rs_s);
-  __syncthreads();
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= lanes * nv) return;
+  const bool active = gid < lanes * nv;
   const int v = gid % nv;
   const int c = v * 8;
+  const bool second = a.x1.base != nullptr && c >= a.c0;
+  const TI* src = reinterpret_cast<const TI*>(second ? a.x1.base : a.x0.base) + (second ? c - a.c0 : c);
+  const int sC = second ? a.x1.C : a.x0.C;
+  TO* dst = reinterpret_cast<TO*>(a.out.base) + c;
+  const int ntok = a.x0.rows * B * W;
+  // the first 4 token vectors are loaded before the statistics prologue (they do not depend on it)
+  float x[4][8];
+  int t0 = gid / nv;
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = t0 + k * lanes;
+      if (t < ntok) load8(src + (long long)t * sC, x[k]);
+    }
+  }
+  gn_prep(a, mu_s, rs_s);
+  __syncthreads();
+  if (!active) return;
   float A[2][8], Bc[2][8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
@@ -213,18 +258,7 @@ __global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a,
       Bc[bb][e] = be - mu_s[bi * G + g] * rs;
     }
   }
-  const bool second = a.x1.base != nullptr && c >= a.c0;
-  const TI* src = reinterpret_cast<const TI*>(second ? a.x1.base : a.x0.base) + (second ? c - a.c0 : c);
-  const int sC = second ? a.x1.C : a.x0.C;
-  TO* dst = reinterpret_cast<TO*>(a.out.base) + c;
-  const int ntok = a.x0.rows * B * W;
-  for (int t0 = gid / nv; t0 < ntok; t0 += 4 * lanes) {
-    float x[4][8];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int t = t0 + k * lanes;
-      if (t < ntok) load8(src + (long long)t * sC, x[k]);
-    }
+  for (;;) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int t = t0 + k * lanes;
@@ -243,6 +277,13 @@ __global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a,
         for (int e = 0; e < 8; ++e) xv[e] = std::is_same<TO, bf16>::value ? silu_bf16out(xv[e]) : silu_f(xv[e]);
       }
       store8(dst + (long long)t * a.out.C, xv);
+    }
+    t0 += 4 * lanes;
+    if (t0 >= ntok) break;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = t0 + k * lanes;
+      if (t < ntok) load8(src + (long long)t * sC, x[k]);
     }
   }
 }

@@ -872,18 +872,37 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           return a;
         };
         {
+          // few partial slots (small producer grids, the n >= 4 shapes) and no synchronous exchange of
+          // this step's sums: the apply kernel sums the slots itself (no finalize launch) and publishes
+          // m[par]; the asynchronous exchange of m[par] then follows the apply
+          constexpr int MERGE_MAX_SLOTS = 48;
+          const bool can_merge = n == 1 || !sync;
+          std::vector<int> merged(nr, 0);
           for (int vr = 0; vr < nr && do_op; ++vr) {
             const int slots = P.gn_slots[(size_t)vr * P.gns.size() + op.xid];
+            if (slots > 0 && can_merge && slots <= MERGE_MAX_SLOTS) { merged[vr] = slots; continue; }
             if (slots > 0)
               launch_gn_finalize(reinterpret_cast<const double*>(P.rm[vr].arena + P.off_epart), slots, P.B,
                                  reinterpret_cast<double*>(P.rm[vr].arena + gx.off_m[par]), s);
-            else
+            else if (can_merge && gx.nchunk <= MERGE_MAX_SLOTS) {
+              launch_gn_stats(stats_args(vr), s, false);
+              merged[vr] = -gx.nchunk;              // slots of the stats kernel
+            } else
               launch_gn_stats(stats_args(vr), s);
-            P.launches_per_step += slots > 0 ? 1 : 2;
           }
-          if (xo >= 0) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
-          for (int vr = 0; vr < nr && do_op; ++vr) launch_gn_apply(apply_args(vr), s);
-          if (do_op) P.launches_per_step += nr;
+          if (xo >= 0 && !can_merge) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
+          for (int vr = 0; vr < nr && do_op; ++vr) {
+            GnApplyArgs a = apply_args(vr);
+            char* base = P.rm[vr].arena;
+            if (merged[vr] > 0) {
+              a.part = reinterpret_cast<const double*>(base + P.off_epart); a.nslots = merged[vr];
+            } else if (merged[vr] < 0) {
+              a.part = reinterpret_cast<const double*>(base + gx.off_part); a.nslots = -merged[vr];
+            }
+            if (a.nslots) a.m_write = reinterpret_cast<double*>(base + gx.off_m[par]);
+            launch_gn_apply(a, s);
+          }
+          if (xo >= 0 && can_merge) { pcpp_status st = exchange(P, xo, sync, par); if (st != PCPP_OK) return st; }
         }
         break;
       }

@@ -11,8 +11,9 @@ from tools.graph_timing import g_conv
 
 SHAPES = [(4, 32, 1280, 1280, 1, 1), (32, 32, 1280, 1280, 1, 1), (32, 32, 1280, 3840, 1, 1), (4, 32, 1280, 1280, 9, 1),
           (2, 32, 64, 64, 1, 1)]
+EPI = os.environ.get("EPI", "bias")          # epilogue operands: none | bias | bias+temb | bias+temb+res
 for sh in SHAPES:
-    ms, tf = g_conv(*sh)
+    ms, tf = g_conv(*sh, res="res" in EPI, bias="bias" in EPI, temb="temb" in EPI)
     n, tr = pcpp.pcpp_debug_gemm_trace()
     tr = tr.astype(np.float64)
     launches = []
@@ -21,7 +22,7 @@ for sh in SHAPES:
         used = t[:, 0] > 0
         launches.append(t[used])
     launches.sort(key=lambda t: t[:, 0].min())
-    print(f"shape rows={sh[0]} W={sh[1]} K={sh[2]} N={sh[3]} taps={sh[4]}: {ms * 1e3:.2f} us/launch ({tf:.0f} TF/s), CTAs={len(launches[-1])}")
+    print(f"[{EPI}] shape rows={sh[0]} W={sh[1]} K={sh[2]} N={sh[3]} taps={sh[4]}: {ms * 1e3:.2f} us/launch ({tf:.0f} TF/s), CTAs={len(launches[-1])}")
     prev_end = None
     for t in launches:
         e = t[:, 0].min()

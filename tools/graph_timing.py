@@ -34,14 +34,15 @@ def g_attn(h, W, C, rows, B=2):
     return _time_graph(lambda st: pcpp.pcpp_op_attention(q, kvs, list(rows), h, B, W, C, o, stream=st))
 
 
-def g_conv(rows, W, Cin, Cout, taps, stride, res=False, B=2):
+def g_conv(rows, W, Cin, Cout, taps, stride, res=False, B=2, bias=True, temb=False):
     pad = 1 if taps == 9 else 0
     x = torch.randn(rows + 2 * pad, B, W, Cin, device="cuda").bfloat16()
     w = (torch.randn(Cout, taps * Cin, device="cuda") / (taps * Cin) ** 0.5).bfloat16()
     y = torch.empty(rows // stride, B, W // stride, Cout, device="cuda", dtype=torch.bfloat16)
     r = torch.randn_like(y) if res else None
-    b = torch.zeros(Cout, device="cuda")
-    ms = _time_graph(lambda st: pcpp.pcpp_op_conv(x, rows, B, W, Cin, taps, stride, w, b, None, r, y, Cout, stream=st))
+    b = torch.zeros(Cout, device="cuda") if bias else None
+    t = torch.zeros(B, Cout, device="cuda") if temb else None
+    ms = _time_graph(lambda st: pcpp.pcpp_op_conv(x, rows, B, W, Cin, taps, stride, w, b, t, r, y, Cout, stream=st))
     return ms, 2.0 * (rows // stride) * B * (W // stride) * Cout * taps * Cin / (ms * 1e-3) / 1e12
 
 
