@@ -44,11 +44,10 @@ struct TcGemmParams {
 
 };
 
-// Extra shared memory of the stats-fused variant: per epilogue warp a 32 x 17-word bf16 transpose
-// tile (conflict-free row writes / column reads) and the warp's [2][32][2] fp64 group accumulators
-// (fp64 across tiles: the E[x^2] - mu^2 form loses digits when a group's mean is large against its std).
-constexpr int ST_TILE_WORDS = 32 * 17;
-constexpr int ST_SMEM = 4 * ST_TILE_WORDS * 4 + 4 * 128 * 8;
+// The stats-fused variant (ST) needs no extra shared memory: the group accumulators live in
+// registers (lane g owns group g) and the column sums are read back from the staging tile, so ST
+// GEMMs keep the same ring depth as the plain ones.
+constexpr int ST_SMEM = 0;
 
 // Epilogue output staging: per epilogue warp one 32-row x 32-column bf16 tile (2 KB, SWIZZLE_64B
 // layout) that a TMA store writes out -- coalesced, asynchronous stores instead of one 64-byte
@@ -117,57 +116,13 @@ __device__ __forceinline__ void res_prefetch(const TcGemmParams& p, long long rr
   pre[4] = make_uint4(__float_as_uint(bl), __float_as_uint(t0), __float_as_uint(t1), 0u);
 }
 
-// Fused GroupNorm statistics of one 32-column chunk held by a warp (lane = row, u = the row's 32
-// bf16 outputs as stored): transpose through smem so lane j sums column j over the 32 rows, then a
-// segmented suffix scan over lanes of the same group; the group's first lane adds into the warp's
-// accumulator sacc[b][g][{sum, sumsq}].  Fixed order everywhere (deterministic).
-__device__ __forceinline__ void gn_chunk_stats(uint32_t* stile, double* sacc, const uint32_t* u, int b, unsigned bmask,
-                                               int col0, int cg) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) stile[lane * 17 + i] = u[i];
-  __syncwarp();
-  const int sh = (lane & 1) * 16, wj = lane >> 1;
-  float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
-  const bool mixed = bmask != 0u && bmask != 0xffffffffu;
-  if (!mixed) {
-#pragma unroll 8
-    for (int rr = 0; rr < 32; ++rr) {
-      const float x = __uint_as_float((stile[rr * 17 + wj] >> sh) << 16);
-      s0 += x; q0 = fmaf(x, x, q0);
-    }
-  } else {
-#pragma unroll 8
-    for (int rr = 0; rr < 32; ++rr) {
-      const float x = __uint_as_float((stile[rr * 17 + wj] >> sh) << 16);
-      if ((bmask >> rr) & 1u) { s1 += x; q1 = fmaf(x, x, q1); } else { s0 += x; q0 = fmaf(x, x, q0); }
-    }
-  }
-  __syncwarp();                                   // stile is rewritten by the next chunk
-  const int col = col0 + lane;
-  const int g = col / cg;
-  const int rem = cg - 1 - (col - g * cg);        // columns after this one in the same group
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const float t0 = __shfl_down_sync(0xffffffffu, s0, d), t1 = __shfl_down_sync(0xffffffffu, q0, d);
-    const float t2 = __shfl_down_sync(0xffffffffu, s1, d), t3 = __shfl_down_sync(0xffffffffu, q1, d);
-    if (d <= rem && lane + d < 32) { s0 += t0; q0 += t1; s1 += t2; q1 += t3; }
-  }
-  if (lane == 0 || rem == cg - 1) {
-    if (!mixed) {
-      double* a = sacc + (b * 32 + g) * 2;
-      a[0] += s0; a[1] += q0;
-    } else {
-      double* a = sacc + g * 2;
-      a[0] += s0; a[1] += q0; a[64] += s1; a[65] += q1;
-    }
-  }
-  __syncwarp();
-}
-
-// The same statistics read from the warp's SWIZZLE_64B staging tile (row rr = 64 B; 16-byte chunk j of
-// the row at chunk j ^ ((rr >> 1) & 3)): no extra transpose writes.
-__device__ __forceinline__ void gn_chunk_stats_stg(const uint8_t* stg, double* sacc, int b, unsigned bmask, int col0, int cg) {
+// Fused GroupNorm statistics of one 32-column chunk held by a warp, read from its SWIZZLE_64B staging
+// tile (row rr = 64 B; 16-byte chunk j of the row at chunk j ^ ((rr >> 1) & 3)): lane j sums column j
+// over the 32 rows, a segmented suffix scan over lanes of the same group leaves each group's chunk sums
+// at its first lane, and the owner lane g (acc: group g's {sum, sumsq} per CFG branch, fp64 registers)
+// adds them.  Fixed order everywhere (deterministic).
+struct GnAcc { double s0, q0, s1, q1; };   // CFG branch b = 0 / 1 (named: no local-memory indexing)
+__device__ __forceinline__ void gn_chunk_stats_stg(const uint8_t* stg, GnAcc& acc, int b, unsigned bmask, int col0, int cg) {
   const int lane = threadIdx.x & 31;
   const int sh = (lane & 1) * 16, wj = lane >> 1;
   const uint32_t* t32 = reinterpret_cast<const uint32_t*>(stg);
@@ -188,16 +143,17 @@ __device__ __forceinline__ void gn_chunk_stats_stg(const uint8_t* stg, double* s
     const float t2 = __shfl_down_sync(0xffffffffu, s1, d), t3 = __shfl_down_sync(0xffffffffu, q1, d);
     if (d <= rem && lane + d < 32) { s0 += t0; q0 += t1; s1 += t2; q1 += t3; }
   }
-  if (lane == 0 || rem == cg - 1) {
-    if (!mixed) {
-      double* a = sacc + (b * 32 + g) * 2;
-      a[0] += s0; a[1] += q0;
-    } else {
-      double* a = sacc + g * 2;
-      a[0] += s0; a[1] += q0; a[64] += s1; a[65] += q1;
-    }
+  // owner lane g <- the first lane of group g in this chunk (if the group intersects it)
+  const int first = max(lane * cg, col0);
+  const bool present = first < col0 + 32 && first < (lane + 1) * cg;
+  const int src = present ? first - col0 : 0;
+  const float v0 = __shfl_sync(0xffffffffu, s0, src), v1 = __shfl_sync(0xffffffffu, q0, src);
+  const float v2 = __shfl_sync(0xffffffffu, s1, src), v3 = __shfl_sync(0xffffffffu, q1, src);
+  if (present) {
+    if (mixed) { acc.s0 += v0; acc.q0 += v1; acc.s1 += v2; acc.q1 += v3; }
+    else if (b) { acc.s1 += v0; acc.q1 += v1; }
+    else { acc.s0 += v0; acc.q0 += v1; }
   }
-  __syncwarp();
 }
 
 __device__ __forceinline__ long long res_row(const TcGemmParams& p, int r, int b, int w, int n0) {
@@ -207,7 +163,7 @@ __device__ __forceinline__ long long res_row(const TcGemmParams& p, int r, int b
 // rres0: chunk 0's epilogue operands, prefetched by the caller before it waited for the accumulator
 template <int BN, bool ST>
 __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t tacc, int r, int b, int w, bool valid,
-                                              int n0, int z, uint32_t* stile, double* sacc, unsigned bmask,
+                                              int n0, int z, GnAcc& gacc, unsigned bmask,
                                               const uint4* rres0, uint8_t* stg) {
   const bool second = n0 >= p.n_split;
   const ActView& ov = second ? p.out2 : p.out;
@@ -298,7 +254,7 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
       for (int j = 0; j < 4; ++j) rowp[j ^ sw] = make_uint4(uo[4 * j], uo[4 * j + 1], uo[4 * j + 2], uo[4 * j + 3]);
       sm100::fence_proxy_async_smem();
       __syncwarp();
-      if constexpr (ST) gn_chunk_stats_stg(stg, sacc, b, bmask, n0 + c, p.gn_cg);
+      if constexpr (ST) gn_chunk_stats_stg(stg, gacc, b, bmask, n0 + c, p.gn_cg);
       // a warp whose first row lies past the tile's tokens (W < 128 without whole-row tiles) stores
       // nothing: its box would land on the next row; otherwise rows past W are clipped by the TMA
       if (lane == 0 && ((threadIdx.x >> 5) & 3) * 32 < p.Wbox * p.Bbox * p.Rbox) {   // warp q: rows 32 q ..
@@ -313,31 +269,7 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
       uint32_t v[32];
       sm100::tmem_ld32(tacc + c, v);
       sm100::tmem_wait_ld();
-      if constexpr (ST) {
-        // stats variant (bf16 out, no second output): every lane takes part in the warp transpose
-        uint32_t uo[16];
-        float f[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-        epilogue_math(p, f, b, rcur, valid);
-        if (valid) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
-            uo[i] = *reinterpret_cast<uint32_t*>(&h2);
-          }
-          uint4* po = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(ov.base) + orow + c);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) po[j] = make_uint4(uo[4 * j], uo[4 * j + 1], uo[4 * j + 2], uo[4 * j + 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) uo[i] = 0u;
-        }
-        gn_chunk_stats(stile, sacc, uo, b, bmask, n0 + c, p.gn_cg);
-#pragma unroll
-        for (int j = 0; j < EPI_PRE; ++j) rcur[j] = rnext[j];
-        continue;
-      }
+      // (ST GEMMs always take the staged path: launch_gemm_tc_cfg fuses the statistics only there)
       float f[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
@@ -367,13 +299,19 @@ __device__ __forceinline__ void trace_stamp(const TcGemmParams& p, int i) {
 }
 
 // End of a stats-fused GEMM (epilogue warps 2-5 only, named barrier 1): the 4 warps' fp64 group
-// accumulators -> this CTA's slot, fixed order (gn_finalize then sums gridDim.x slots, not 4x as many).
+// accumulators (registers of lanes 0..31) -> smem scratch (the staging area: every warp has waited for
+// its stores to read it) -> this CTA's slot, fixed order (gn_finalize then sums gridDim.x slots).
 // Folding that finalize into the last CTA to arrive (fence + ticket + slot reduction) was measured
 // slower than the separate launch: +6 us per GEMM of tail against ~2 us for the PDL-launched finalize.
-__device__ __forceinline__ void gn_cta_finish(const TcGemmParams& p, const double* st_acc) {
+__device__ __forceinline__ void gn_cta_finish(const TcGemmParams& p, const GnAcc& acc, uint8_t* scratch) {
+  const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3;
+  double* st = reinterpret_cast<double*>(scratch);                 // [4 warps][b][g][k] = 4 KB
+  asm volatile("bar.sync 1, 128;" ::: "memory");                   // every warp is done with the staging area
+  st[q * 128 + (0 * 32 + lane) * 2 + 0] = acc.s0; st[q * 128 + (0 * 32 + lane) * 2 + 1] = acc.q0;
+  st[q * 128 + (1 * 32 + lane) * 2 + 0] = acc.s1; st[q * 128 + (1 * 32 + lane) * 2 + 1] = acc.q1;
   asm volatile("bar.sync 1, 128;" ::: "memory");
-  const int t = threadIdx.x - 64;                      // 0..127 = (b, g, {sum, sumsq})
-  p.gn_part[(size_t)blockIdx.x * 128 + t] = ((st_acc[t] + st_acc[128 + t]) + st_acc[256 + t]) + st_acc[384 + t];
+  const int t = threadIdx.x - 64;                                  // 0..127 = (b, g, {sum, sumsq})
+  p.gn_part[(size_t)blockIdx.x * 128 + t] = ((st[t] + st[128 + t]) + st[256 + t]) + st[384 + t];
 }
 
 // Cluster split-K epilogue (epilogue warps): CTA z of the cluster owns rows [z R, (z + 1) R) of the
@@ -381,7 +319,7 @@ __device__ __forceinline__ void gn_cta_finish(const TcGemmParams& p, const doubl
 // the csplit partial tiles of its rows through DSMEM in cluster-rank order (fixed: deterministic),
 // then bias / temb / residual, the staged TMA store and the GroupNorm statistics as the plain path.
 template <int BN, bool ST, typename Decode>
-__device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_t* smem, uint8_t* stg_all, double* st_acc,
+__device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_t* smem, uint8_t* stg_all,
                                                    const Decode& decode) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = warp & 3;
   const int S = p.csplit, R = 128 / S, nrb = R / 32, wpr = 4 / nrb;
@@ -394,7 +332,7 @@ __device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_
   const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
   const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
   const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
-  double* sacc = st_acc + q * 128;
+  GnAcc gacc = {0.0, 0.0, 0.0, 0.0};
   uint8_t* stg = stg_all + q * 2048;
   const bool second = n0 >= p.n_split;
   const int ncol0 = second ? n0 - p.n_split : n0;
@@ -432,14 +370,14 @@ __device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_
     for (int j = 0; j < 4; ++j) rowp[j ^ sw] = make_uint4(uo[4 * j], uo[4 * j + 1], uo[4 * j + 2], uo[4 * j + 3]);
     sm100::fence_proxy_async_smem();
     __syncwarp();
-    if constexpr (ST) gn_chunk_stats_stg(stg, sacc, b, bmask, n0 + c, p.gn_cg);
+    if constexpr (ST) gn_chunk_stats_stg(stg, gacc, b, bmask, n0 + c, p.gn_cg);
     if (lane == 0 && (int)z * R + rb * 32 < p.Wbox * p.Bbox * p.Rbox) {
       sm100::tma_store_4d(mo, stg, ncol0 + c, wq, bq, rq);
       sm100::bulk_commit();
     }
   }
   if (lane == 0) sm100::bulk_wait<0>();
-  if (ST) gn_cta_finish(p, st_acc);
+  if (ST) gn_cta_finish(p, gacc, stg_all);
 }
 
 template <int BN, bool ST>
@@ -462,8 +400,6 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   uint64_t* tempty = tfull + 2;              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint8_t* stg_all = smem + Cfg::STAGES * Cfg::STAGE + 1024;                                 // 4 x 2 KB staging
-  uint32_t* st_tile = reinterpret_cast<uint32_t*>(stg_all + STG_BYTES);                        // ST only
-  double* st_acc = reinterpret_cast<double*>(st_tile + 4 * ST_TILE_WORDS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -561,13 +497,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
     const int q = warp & 3;
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
-    uint32_t* stile = st_tile + q * ST_TILE_WORDS;
-    double* sacc = st_acc + q * 128;
-    if (ST) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) sacc[lane * 4 + i] = 0.0;
-      __syncwarp();
-    }
+    GnAcc gacc = {0.0, 0.0, 0.0, 0.0};   // ST: lane g's group-g sums
     int tc = 0;
     if (p.csplit > 1) {
       // cluster split-K: this CTA's fp32 partial tile -> its smem (the ring is free: every MMA of this
@@ -600,18 +530,18 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       sm100::fence_after();
       if (tc == 0 && threadIdx.x == 64) trace_stamp(p, 4);
       const uint32_t tacc = tmem + a * BN + (uint32_t(q * 32) << 16);
-      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, stile, sacc, bmask, rres0, stg_all + q * 2048);
+      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, gacc, bmask, rres0, stg_all + q * 2048);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
     }
     if (p.tma_st && lane == 0) sm100::bulk_wait<0>();   // staged stores complete before exit
     if (threadIdx.x == 64) trace_stamp(p, 5);
-    if (ST && p.csplit <= 1) gn_cta_finish(p, st_acc);
+    if (ST && p.csplit <= 1) gn_cta_finish(p, gacc, stg_all);
   }
   if (p.csplit > 1) {
     sm100::cluster_sync();                    // every CTA's partial tile is in its smem
-    if (warp >= 2) gemm_csplit_reduce<BN, ST>(p, smem, stg_all, st_acc, decode);
+    if (warp >= 2) gemm_csplit_reduce<BN, ST>(p, smem, stg_all, decode);
     sm100::cluster_sync();                    // the peers' smem stays alive until every CTA has read it
   }
   sm100::fence_before();
@@ -762,8 +692,6 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
   uint64_t* tempty = tfull + 2;              // [2] (leader's counts both CTAs' epilogue warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint8_t* stg_all = smem + Cfg::STAGES * Cfg::STAGE + 1024;                                 // 4 x 2 KB staging
-  uint32_t* st_tile = reinterpret_cast<uint32_t*>(stg_all + STG_BYTES);                        // ST only
-  double* st_acc = reinterpret_cast<double*>(st_tile + 4 * ST_TILE_WORDS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_rank();
@@ -860,13 +788,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
     const int q = warp & 3;
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
-    uint32_t* stile = st_tile + q * ST_TILE_WORDS;
-    double* sacc = st_acc + q * 128;
-    if (ST) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) sacc[lane * 4 + i] = 0.0;
-      __syncwarp();
-    }
+    GnAcc gacc = {0.0, 0.0, 0.0, 0.0};   // ST: lane g's group-g sums
     int tc = 0;
     for (int u = cid; u < units; u += ncl, ++tc) {
       int r0, b0, w0, n0, z;
@@ -879,14 +801,14 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
       const int a = tc & 1;
       sm100::mbar_wait_cluster(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
-      gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, stile, sacc, bmask, rres0,
+      gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, gacc, bmask, rres0,
                             stg_all + q * 2048);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
     }
     if (p.tma_st && lane == 0) sm100::bulk_wait<0>();
-    if (ST) gn_cta_finish(p, st_acc);
+    if (ST) gn_cta_finish(p, gacc, stg_all);
   }
   sm100::fence_before();
   sm100::cluster_sync();
@@ -1064,7 +986,7 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   // GroupNorm statistics ride on the epilogue of an unsplit GEMM; a split-K GEMM leaves them to the
   // consumer GN's own statistics pass (gn_slots = 0)
   if (p.csplit > 1 && !p.tma_st) return false;      // the cluster reduction stores through the TMA path
-  const bool st = gn_fusable(g) && (p.splits == 1 || p.csplit > 1);
+  const bool st = gn_fusable(g) && (p.splits == 1 || p.csplit > 1) && p.tma_st;   // the stats read the staging tile
   if (st) { p.gn_part = g.gn_part; p.gn_cg = g.N / 32; }
   else if (g.gn_slots) *g.gn_slots = 0;
   if (pair) {
