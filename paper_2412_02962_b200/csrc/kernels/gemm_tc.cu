@@ -7,8 +7,9 @@
 //   filled by the stale-halo exchange, reading D8), columns outside [0, W) are zero-filled by TMA.
 //   The concat input of up-block 1x1 skips is two K ranges from two tensor maps (no concat copy).
 // * B (weights [N][taps*Cin], K-major) is a 2-D TMA box (64, BN).
-// * Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (one elected thread issues
-//   tcgen05.mma 128 x BN x 16), warps 2-5 epilogue (tcgen05.ld -> fused bias/temb/residual -> bf16).
+// * Warp roles (64 + 32 EPI_WARPS threads): warp 0 TMA producer, warp 1 MMA issuer (one elected thread
+//   issues tcgen05.mma 128 x BN x 16), warps 2.. epilogue (tcgen05.ld -> fused bias/temb/residual -> bf16):
+//   two warps per TMEM lane quadrant (warp % 4), each taking every other 32-column chunk.
 // * SWIZZLE_128B K-major smem tiles, STAGES-deep mbarrier ring between TMA and MMA.
 #include <cuda.h>
 #include <cstdio>
@@ -52,7 +53,13 @@ constexpr int ST_SMEM = 0;
 // Epilogue output staging: per epilogue warp one 32-row x 32-column bf16 tile (2 KB, SWIZZLE_64B
 // layout) that a TMA store writes out -- coalesced, asynchronous stores instead of one 64-byte
 // segment per thread and row (measured 2.6 us per 128 x 160 tile with row-per-thread stores).
-constexpr int STG_BYTES = 4 * 2048;
+// Epilogue warps: 2 per TMEM lane quadrant.  One warp per quadrant left the epilogue latency-bound
+// (~900 clk per 32-column chunk: a dependent tcgen05.ld -> math -> smem -> store chain with nothing to
+// interleave on its scheduler); the second warp of a quadrant takes the odd chunks.
+constexpr int EPI_WARPS = 8;
+constexpr int EPI_HALVES = EPI_WARPS / 4;
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int STG_BYTES = EPI_WARPS * 2048;
 // smem: [ring][barriers (1 KB)][staging 8 KB][ST: transpose tiles + accumulators]; <= 227 KB in all
 constexpr int SMEM_FIXED = 1024 /*align slack*/ + 1024 + STG_BYTES;
 constexpr int SMEM_MAX = 232448;
@@ -161,10 +168,12 @@ __device__ __forceinline__ long long res_row(const TcGemmParams& p, int r, int b
 }
 
 // rres0: chunk 0's epilogue operands, prefetched by the caller before it waited for the accumulator
+// h: this warp's half of the quadrant -- chunks c = 32 h, 32 (h + EPI_HALVES), ...
 template <int BN, bool ST>
 __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t tacc, int r, int b, int w, bool valid,
                                               int n0, int z, GnAcc& gacc, unsigned bmask,
-                                              const uint4* rres0, uint8_t* stg) {
+                                              const uint4* rres0, uint8_t* stg, int h) {
+  constexpr int CSTEP = 32 * EPI_HALVES;
   const bool second = n0 >= p.n_split;
   const ActView& ov = second ? p.out2 : p.out;
   const int ncol0 = second ? n0 - p.n_split : n0;
@@ -179,7 +188,7 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
 #pragma unroll 1
     for (int c = 0; c < BN; c += 128) {
 #pragma unroll 1
-      for (int hh = 0; hh < 64; hh += 32) {
+      for (int hh = 32 * h; hh < 64; hh += CSTEP) {
         uint32_t va[32], vg[32];
         sm100::tmem_ld32(tacc + c + hh, va);
         sm100::tmem_ld32(tacc + c + 64 + hh, vg);
@@ -211,7 +220,7 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
     const long long T = ((long long)r * p.B + b) * p.w_out + w;
     float* wp = p.ws + ((long long)z * p.rows_out * p.B * p.w_out + T) * p.N + n0;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 32 * h; c < BN; c += CSTEP) {
       uint32_t v[32];
       sm100::tmem_ld32(tacc + c, v);
       sm100::tmem_wait_ld();
@@ -229,8 +238,8 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
     uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 64);
     const int sw = (lane >> 1) & 3;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      if (c + 32 < BN) res_prefetch(p, rrow, n0, c + 32, valid, rnext);
+    for (int c = 32 * h; c < BN; c += CSTEP) {
+      if (c + CSTEP < BN) res_prefetch(p, rrow, n0, c + CSTEP, valid, rnext);
       uint32_t v[32];
       sm100::tmem_ld32(tacc + c, v);
       sm100::tmem_wait_ld();
@@ -264,8 +273,8 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
     }
   } else {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      if (c + 32 < BN) res_prefetch(p, rrow, n0, c + 32, valid, rnext);
+    for (int c = 32 * h; c < BN; c += CSTEP) {
+      if (c + CSTEP < BN) res_prefetch(p, rrow, n0, c + CSTEP, valid, rnext);
       uint32_t v[32];
       sm100::tmem_ld32(tacc + c, v);
       sm100::tmem_wait_ld();
@@ -304,14 +313,19 @@ __device__ __forceinline__ void trace_stamp(const TcGemmParams& p, int i) {
 // Folding that finalize into the last CTA to arrive (fence + ticket + slot reduction) was measured
 // slower than the separate launch: +6 us per GEMM of tail against ~2 us for the PDL-launched finalize.
 __device__ __forceinline__ void gn_cta_finish(const TcGemmParams& p, const GnAcc& acc, uint8_t* scratch) {
-  const int lane = threadIdx.x & 31, q = (threadIdx.x >> 5) & 3;
-  double* st = reinterpret_cast<double*>(scratch);                 // [4 warps][b][g][k] = 4 KB
-  asm volatile("bar.sync 1, 128;" ::: "memory");                   // every warp is done with the staging area
-  st[q * 128 + (0 * 32 + lane) * 2 + 0] = acc.s0; st[q * 128 + (0 * 32 + lane) * 2 + 1] = acc.q0;
-  st[q * 128 + (1 * 32 + lane) * 2 + 0] = acc.s1; st[q * 128 + (1 * 32 + lane) * 2 + 1] = acc.q1;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const int lane = threadIdx.x & 31, e = (threadIdx.x >> 5) - 2;
+  double* st = reinterpret_cast<double*>(scratch);                 // [EPI_WARPS][b][g][k] = 1 KB per warp
+  asm volatile("bar.sync 1, %0;" :: "n"(32 * EPI_WARPS) : "memory");   // every warp is done with the staging area
+  st[e * 128 + (0 * 32 + lane) * 2 + 0] = acc.s0; st[e * 128 + (0 * 32 + lane) * 2 + 1] = acc.q0;
+  st[e * 128 + (1 * 32 + lane) * 2 + 0] = acc.s1; st[e * 128 + (1 * 32 + lane) * 2 + 1] = acc.q1;
+  asm volatile("bar.sync 1, %0;" :: "n"(32 * EPI_WARPS) : "memory");
   const int t = threadIdx.x - 64;                                  // 0..127 = (b, g, {sum, sumsq})
-  p.gn_part[(size_t)blockIdx.x * 128 + t] = ((st[t] + st[128 + t]) + st[256 + t]) + st[384 + t];
+  if (t < 128) {
+    double v = st[t];
+#pragma unroll
+    for (int k = 1; k < EPI_WARPS; ++k) v += st[k * 128 + t];
+    p.gn_part[(size_t)blockIdx.x * 128 + t] = v;
+  }
 }
 
 // Cluster split-K epilogue (epilogue warps): CTA z of the cluster owns rows [z R, (z + 1) R) of the
@@ -321,9 +335,9 @@ __device__ __forceinline__ void gn_cta_finish(const TcGemmParams& p, const GnAcc
 template <int BN, bool ST, typename Decode>
 __device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_t* smem, uint8_t* stg_all,
                                                    const Decode& decode) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = warp & 3;
-  const int S = p.csplit, R = 128 / S, nrb = R / 32, wpr = 4 / nrb;
-  const int rb = q % nrb, cw = q / nrb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, e = warp - 2;
+  const int S = p.csplit, R = 128 / S, nrb = R / 32, wpr = EPI_WARPS / nrb;
+  const int rb = e % nrb, cw = e / nrb;
   const uint32_t z = sm100::cluster_rank();
   int r0, b0, w0, n0, zz;
   decode(blockIdx.x, r0, b0, w0, n0, zz);
@@ -333,7 +347,7 @@ __device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_
   const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
   const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
   GnAcc gacc = {0.0, 0.0, 0.0, 0.0};
-  uint8_t* stg = stg_all + q * 2048;
+  uint8_t* stg = stg_all + e * 2048;
   const bool second = n0 >= p.n_split;
   const int ncol0 = second ? n0 - p.n_split : n0;
   const CUtensorMap* mo = second ? &p.mo2 : &p.mo;
@@ -381,7 +395,7 @@ __device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_
 }
 
 template <int BN, bool ST>
-__global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__ TcGemmParams p) {
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
   if (threadIdx.x == 0) trace_stamp(p, 0);
   // Persistent: CTA c handles work units c, c + gridDim.x, ...; a unit = (m tile, n tile, k split).
@@ -399,13 +413,13 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
   uint64_t* tfull = empty + Cfg::STAGES;     // [2]
   uint64_t* tempty = tfull + 2;              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* stg_all = smem + Cfg::STAGES * Cfg::STAGE + 1024;                                 // 4 x 2 KB staging
+  uint8_t* stg_all = smem + Cfg::STAGES * Cfg::STAGE + 1024;                                 // EPI_WARPS x 2 KB staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&p.ma0); sm100::tma_prefetch(&p.ma1); sm100::tma_prefetch(&p.mb);
     for (int s = 0; s < Cfg::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], EPI_WARPS); }
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -493,8 +507,8 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       trace_stamp(p, 3);
     }
   } else {
-    // epilogue: warp w reads TMEM lanes [32 (w%4), 32 (w%4) + 32)
-    const int q = warp & 3;
+    // epilogue: warp w reads TMEM lanes [32 (w%4), 32 (w%4) + 32), chunk half h = (w - 2) / 4
+    const int q = warp & 3, h = (warp - 2) >> 2;
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
     GnAcc gacc = {0.0, 0.0, 0.0, 0.0};   // ST: lane g's group-g sums
@@ -506,7 +520,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       sm100::fence_after();
       float* part = reinterpret_cast<float*>(smem);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 32 * h; c < BN; c += 32 * EPI_HALVES) {
         uint32_t v[32];
         sm100::tmem_ld32(tmem + c + (uint32_t(q * 32) << 16), v);
         sm100::tmem_wait_ld();
@@ -524,13 +538,13 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(const __grid_constant__
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
       const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
       uint4 rres0[EPI_PRE];
-      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 0, valid, rres0);   // overlaps the main loop
+      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 32 * h, valid, rres0);   // overlaps the main loop
       const int a = tc & 1;
       sm100::mbar_wait(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
       if (tc == 0 && threadIdx.x == 64) trace_stamp(p, 4);
       const uint32_t tacc = tmem + a * BN + (uint32_t(q * 32) << 16);
-      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, gacc, bmask, rres0, stg_all + q * 2048);
+      gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, gacc, bmask, rres0, stg_all + (warp - 2) * 2048, h);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
@@ -639,7 +653,7 @@ static int launch_bn(const TcGemmParams& p, cudaStream_t s) {   // returns the g
   const int units = p.m_tiles * (p.N / BN) * p.splits;
   if (p.csplit > 1) {            // one unit per CTA, clusters of csplit CTAs along K
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(units); cfg.blockDim = dim3(192); cfg.stream = s;
+    cfg.gridDim = dim3(units); cfg.blockDim = dim3(GEMM_THREADS); cfg.stream = s;
     cfg.dynamicSmemBytes = p.gn_part ? TcCfg<BN, true>::SMEM : TcCfg<BN, false>::SMEM;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -653,8 +667,8 @@ static int launch_bn(const TcGemmParams& p, cudaStream_t s) {   // returns the g
     return units;
   }
   const int grid = units < 148 ? units : 148;
-  if (p.gn_part) launch_pdl(gemm_tc_kernel<BN, true>, dim3(grid), dim3(192), TcCfg<BN, true>::SMEM, s, p);
-  else launch_pdl(gemm_tc_kernel<BN, false>, dim3(grid), dim3(192), TcCfg<BN, false>::SMEM, s, p);
+  if (p.gn_part) launch_pdl(gemm_tc_kernel<BN, true>, dim3(grid), dim3(GEMM_THREADS), TcCfg<BN, true>::SMEM, s, p);
+  else launch_pdl(gemm_tc_kernel<BN, false>, dim3(grid), dim3(GEMM_THREADS), TcCfg<BN, false>::SMEM, s, p);
   return grid;
 }
 
@@ -679,7 +693,7 @@ struct TcCfg2 {
 // ST: the epilogue also accumulates the GroupNorm sums of the output (as the 1-CTA kernel); each
 // CTA of the pair owns its 128 rows, so the per-warp partial slots are blockIdx.x * 4 + warp.
 template <int BN, bool ST>
-__global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant__ TcGemmParams p) {
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc2_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
   using Cfg = TcCfg2<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
@@ -691,14 +705,14 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
   uint64_t* tfull = empty + Cfg::STAGES;     // [2]
   uint64_t* tempty = tfull + 2;              // [2] (leader's counts both CTAs' epilogue warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* stg_all = smem + Cfg::STAGES * Cfg::STAGE + 1024;                                 // 4 x 2 KB staging
+  uint8_t* stg_all = smem + Cfg::STAGES * Cfg::STAGE + 1024;                                 // EPI_WARPS x 2 KB staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_rank();
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&p.ma0); sm100::tma_prefetch(&p.ma1); sm100::tma_prefetch(&p.mb);
     for (int s = 0; s < Cfg::STAGES; ++s) { sm100::mbar_init(&full[s], 1); sm100::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 8); }
+    for (int a = 0; a < 2; ++a) { sm100::mbar_init(&tfull[a], 1); sm100::mbar_init(&tempty[a], 2 * EPI_WARPS); }
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc2<Cfg::TMEM_COLS>(tmem_slot);
@@ -785,7 +799,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
       }
     }
   } else {
-    const int q = warp & 3;
+    const int q = warp & 3, h = (warp - 2) >> 2;
     const int m = q * 32 + lane;
     const int wi = m % p.Wbox, bi = (m / p.Wbox) % p.Bbox, ri = m / (p.Wbox * p.Bbox);
     GnAcc gacc = {0.0, 0.0, 0.0, 0.0};   // ST: lane g's group-g sums
@@ -797,12 +811,12 @@ __global__ void __launch_bounds__(192, 1) gemm_tc2_kernel(const __grid_constant_
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
       const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
       uint4 rres0[EPI_PRE];
-      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 0, valid, rres0);
+      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 32 * h, valid, rres0);
       const int a = tc & 1;
       sm100::mbar_wait_cluster(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
       gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, gacc, bmask, rres0,
-                            stg_all + q * 2048);
+                            stg_all + (warp - 2) * 2048, h);
       sm100::fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
@@ -821,7 +835,7 @@ static int launch_bn2(const TcGemmParams& p, cudaStream_t s) {   // returns the 
   const int clusters = units < 74 ? units : 74;
   cudaLaunchConfig_t cfg = {};
   const bool st = p.gn_part != nullptr;
-  cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(192);
+  cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = st ? TcCfg2<BN, true>::SMEM : TcCfg2<BN, false>::SMEM; cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
