@@ -242,6 +242,9 @@ __global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a,
       if (t < ntok) load8(src + (long long)t * sC, x[k]);
     }
   }
+  // the affine parameters are in flight during the statistics prologue too
+  float ga8[8], be8[8];
+  if (active) { load8(a.gamma + c, ga8); load8(a.beta + c, be8); }
   gn_prep(a, mu_s, rs_s);
   __syncthreads();
   if (!active) return;
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a,
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int g = (c + e) / cg;
-    const float ga = a.gamma[c + e], be = a.beta[c + e];
+    const float ga = ga8[e], be = be8[e];
 #pragma unroll
     for (int bb = 0; bb < 2; ++bb) {
       const int bi = bb < B ? bb : 0;
