@@ -40,12 +40,6 @@ struct GemmArgs {
   // [value 64 | gate 64] (the builder interleaves W_ff1's rows); out gets N / 2 columns
   // out[:, 64 k + j] = (D[:, 128 k + j] + bias) * gelu(D[:, 128 k + 64 + j] + bias)
   int geglu = 0;
-  // optional early start behind the producing attention (tcgen05 path only): the GEMM does not wait
-  // for the previous kernel's completion; the TMA producer waits (acquire, gpu scope) until
-  // row_wait[r] >= row_target for every input row r of a tile before loading it, and the epilogue
-  // reads the residual only after the accumulator is ready.  The last CTA to finish zeroes
-  // row_wait[0, rows_out) and *row_ticket (so the next execution starts from zero).
-  unsigned* row_wait = nullptr; unsigned row_target = 0; unsigned* row_ticket = nullptr;
 };
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 
@@ -65,10 +59,6 @@ struct AttnArgs {
   void* out = nullptr;        // [h][B][W][C]
   int dtype = 0;
   float* ws = nullptr; size_t ws_elems = 0;   // split-KV fp32 workspace (optional)
-  // optional row-completion handoff to the consumer GEMM (tcgen05 path only): every CTA adds 1 to
-  // row_done[r] (release, gpu scope) for each query row r it covered, after its output is stored;
-  // a row is complete at heads * B * (column tiles per row) arrivals (GemmArgs::row_wait)
-  unsigned* row_done = nullptr;
 };
 void launch_attn_simt(const AttnArgs& a, cudaStream_t s);
 

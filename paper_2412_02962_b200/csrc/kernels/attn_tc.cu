@@ -32,8 +32,6 @@ struct TcAttnParams {
   void* out;
   int nsplit;                 // split-KV: blockIdx.z = b * nsplit + split; partials -> ws
   float* ws;                  // [nsplit][B][heads][h*W][64 + 2] (O unnormalised, m, l)
-  unsigned* row_done;         // AttnArgs::row_done (null: off)
-  int heads;                  // C / 64
 };
 
 namespace {
@@ -106,17 +104,9 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // 1-D grid.  Default order: query tile fastest (the CTAs of one (b, head) run together and share
-  // its K/V in L2), then head, then (batch, split).  With row_done: head fastest, then (batch, split),
-  // then query tile -- the first query tiles launch and finish first, so the consumer started early
-  // behind this kernel finds its first rows complete while the last wave still runs.
+  const int head = blockIdx.y, b = blockIdx.z / p.nsplit, sp = blockIdx.z % p.nsplit;
   const int nqt = ((p.h + p.Rbox - 1) / p.Rbox) * p.nWt;
-  const int ncta_q = (nqt + NWG - 1) / NWG;
-  int head, bz, qtc;
-  if (p.row_done) { head = blockIdx.x % p.heads; bz = (blockIdx.x / p.heads) % (p.B * p.nsplit); qtc = blockIdx.x / (p.heads * p.B * p.nsplit); }
-  else { qtc = blockIdx.x % ncta_q; head = (blockIdx.x / ncta_q) % p.heads; bz = blockIdx.x / (ncta_q * p.heads); }
-  const int b = bz / p.nsplit, sp = bz % p.nsplit;
-  const int qt0 = NWG * qtc;
+  const int qt0 = NWG * blockIdx.x;
   const int nwg = min(NWG, nqt - qt0);              // query tiles in this CTA
 
   if (warp == 0 && lane == 0) {
@@ -366,10 +356,6 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
           sm100::tma_store_4d(&p.mo, Qs, head * 64, (qt % p.nWt) * p.Wbox, b, (qt / p.nWt) * p.Rbox);
           sm100::bulk_commit();
           sm100::bulk_wait<0>();
-          if (p.row_done) {                     // this tile's rows are stored: hand them to the consumer
-            const int r0 = (qt / p.nWt) * p.Rbox, r1 = min(p.h, r0 + p.Rbox);
-            for (int rr = r0; rr < r1; ++rr) sm100::flag_release_add(p.row_done + rr, 1u);
-          }
         }
       } else if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
         const float inv = 1.f / l;
@@ -440,9 +426,7 @@ bool launch_attn_tc(const AttnArgs& a, cudaStream_t s) {
   // the 1024^2 step than one CTA with two ping-pong warpgroups, and faster than split-KV + combine
   // at every 1024^2 shape (round-1 A/B)
   p.nsplit = 1; p.ws = a.ws;
-  p.heads = a.C / 64;
-  p.row_done = a.row_done;
-  dim3 grid(qtiles * p.heads * a.B);
+  dim3 grid(qtiles, a.C / 64, a.B);
   launch_pdl(attn_tc_kernel<1>, grid, dim3(AttnCfg<1>::THREADS), AttnCfg<1>::SMEM, s, p);
   return true;
 }

@@ -32,9 +32,6 @@ void launch_gemm_auto(const GemmArgs& g, bool allow_tc, cudaStream_t s) {
   if (allow_tc && launch_conv_in(g, s)) return;          // Cin = 4 latent conv (bf16 mode)
   if (allow_tc) ++g_simt_fallbacks;
   launch_gemm_simt(g, s);
-  // an early-start GEMM that could not run on the tensor cores: the SIMT kernel waited for the
-  // attention as usual; reset the row flags it would have reset
-  if (g.row_wait) cudaMemsetAsync(g.row_wait, 0, ((size_t)g.rows_out + 1) * sizeof(unsigned), s);
 }
 bool attn_tc_supported(const AttnArgs& a);
 bool launch_attn_tc(const AttnArgs& a, cudaStream_t s);

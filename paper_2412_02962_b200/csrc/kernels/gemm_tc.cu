@@ -42,9 +42,6 @@ struct TcGemmParams {
   int tma_st;                 // 1: the epilogue stores through smem staging + TMA (bf16 out, Wbox >= 32)
   double* gn_part;            // fused GroupNorm statistics: [gridDim.x CTAs][B=2][G=32][2] fp64
   int gn_cg;                  //   channels per group (N / 32)
-  unsigned* row_wait;         // GemmArgs::row_wait (null: wait for the previous kernel as usual)
-  unsigned row_target;
-  unsigned* row_ticket;
 
 };
 
@@ -306,23 +303,6 @@ __device__ __forceinline__ void gemm_epilogue(const TcGemmParams& p, uint32_t ta
   }
 }
 
-// early start (row_wait): the input rows of a tile are complete (1x1 GEMMs: input rows = output rows)
-__device__ __forceinline__ void rows_wait(const TcGemmParams& p, int r0) {
-  const int r1 = min(p.rows_out, r0 + (p.rowtile ? p.Rbox : 1));
-  for (int r = r0; r < r1; ++r) sm100::flag_wait_geq(p.row_wait + r, p.row_target);
-}
-// the last CTA to finish zeroes the row flags and the ticket for the next execution
-__device__ __forceinline__ void rows_reset(const TcGemmParams& p) {
-  if (!p.row_wait || threadIdx.x != 0) return;
-  __threadfence();
-  if (atomicAdd(p.row_ticket, 1u) == gridDim.x - 1) {
-    __threadfence();
-    for (int r = 0; r < p.rows_out; ++r) p.row_wait[r] = 0u;
-    *p.row_ticket = 0u;
-    __threadfence();
-  }
-}
-
 __device__ __forceinline__ void trace_stamp(const TcGemmParams& p, int i) {
   if (p.trace) {
     unsigned long long t;
@@ -370,7 +350,6 @@ __device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_
   const int r = r0 + ri, b = b0 + bi, w = w0 + wi;
   const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
   const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
-  if (p.row_wait) { if (lane == 0) rows_wait(p, r0); __syncwarp(); }   // acquire: the residual of these rows
   GnAcc gacc = {0.0, 0.0, 0.0, 0.0};
   uint8_t* stg = stg_all + e * STG_WARP;
   const bool second = n0 >= p.n_split;
@@ -453,8 +432,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
   __syncthreads();
   sm100::fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (!p.row_wait) pdl_wait();                  // inputs of this GEMM are produced by the previous kernel
-                                                // (early start: per-tile row flags instead)
+  pdl_wait();                                   // inputs of this GEMM are produced by the previous kernel
   if (threadIdx.x == 0) trace_stamp(p, 1);
 
   const int n_tiles = p.N / BN;
@@ -482,7 +460,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
         int tap = s_begin / p.nkc, kc = s_begin - tap * p.nkc;
         int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
         const int wa = w0 * p.stride, ra = r0 * p.stride + p.pad;
-        if (p.row_wait) rows_wait(p, r0);
         for (int s = s_begin; s < s_end; ++s) {
           sm100::mbar_wait(&empty[st], ph ^ 1);
           sm100::mbar_arrive_expect_tx(&full[st], p.a_bytes + Cfg::B_BYTES);
@@ -566,15 +543,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
       const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
       uint4 rres0[EPI_PRE];
-      if (p.splits <= 1 && !p.row_wait) res_prefetch(p, res_row(p, r, b, w, n0), n0, 32 * h, valid, rres0);   // overlaps the main loop
+      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 32 * h, valid, rres0);   // overlaps the main loop
       const int a = tc & 1;
       sm100::mbar_wait(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
-      if (p.row_wait) {                   // early start: acquire the rows (complete by now), then the residual
-        if (lane == 0) rows_wait(p, r0);
-        __syncwarp();
-        if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 32 * h, valid, rres0);
-      }
       if (tc == 0 && threadIdx.x == 64) trace_stamp(p, 4);
       const uint32_t tacc = tmem + a * BN + (uint32_t(q * 32) << 16);
       gemm_epilogue<BN, ST>(p, tacc, r, b, w, valid, n0, z, gacc, bmask, rres0, stg_all + (warp - 2) * STG_WARP, h);
@@ -594,7 +566,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
   sm100::fence_before();
   __syncthreads();
   if (threadIdx.x == 0) trace_stamp(p, 6);
-  rows_reset(p);
   if (warp == 1) sm100::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
 }
 
@@ -754,7 +725,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc2_kernel(const __grid_
   sm100::cluster_sync();
   sm100::fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (!p.row_wait) pdl_wait();
+  pdl_wait();
 
   const int n_tiles = p.N / BN;
   const int m_pairs = (p.m_tiles + 1) / 2;
@@ -783,7 +754,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc2_kernel(const __grid_
         int dr = p.taps == 9 ? tap / 3 - 1 : 0, dw = p.taps == 9 ? tap % 3 - 1 : 0;
         const int wa = w0 * p.stride, ra = r0 * p.stride + p.pad;
         const int nb = n0 + (int)rank * (BN / 2);
-        if (p.row_wait) rows_wait(p, r0);
         for (int s = s_begin; s < s_end; ++s) {
           sm100::mbar_wait_cluster(&empty[st], ph ^ 1);
           if (rank == 0) sm100::mbar_arrive_expect_tx(&full[st], 2 * (p.a_bytes + Cfg::B_BYTES));
@@ -846,15 +816,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc2_kernel(const __grid_
       const bool valid = (m < p.Wbox * p.Bbox * p.Rbox) && r < p.rows_out && w < p.w_out;
       const unsigned bmask = ST ? __ballot_sync(0xffffffffu, b == 1) : 0u;
       uint4 rres0[EPI_PRE];
-      if (p.splits <= 1 && !p.row_wait) res_prefetch(p, res_row(p, r, b, w, n0), n0, 32 * h, valid, rres0);
+      if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 32 * h, valid, rres0);
       const int a = tc & 1;
       sm100::mbar_wait_cluster(&tfull[a], (tc >> 1) & 1);
       sm100::fence_after();
-      if (p.row_wait) {
-        if (lane == 0) rows_wait(p, r0);
-        __syncwarp();
-        if (p.splits <= 1) res_prefetch(p, res_row(p, r, b, w, n0), n0, 32 * h, valid, rres0);
-      }
       gemm_epilogue<BN, ST>(p, tmem + a * BN + (uint32_t(q * 32) << 16), r, b, w, valid, n0, z, gacc, bmask, rres0,
                             stg_all + (warp - 2) * STG_WARP, h);
       sm100::fence_before();
@@ -866,7 +831,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc2_kernel(const __grid_
   }
   sm100::fence_before();
   sm100::cluster_sync();
-  rows_reset(p);
   if (warp == 1) sm100::tmem_dealloc2<Cfg::TMEM_COLS>(tmem);
 }
 
@@ -1018,10 +982,6 @@ static bool launch_gemm_tc_cfg(const GemmArgs& g, cudaStream_t s, int BN, int wa
   p.res = g.res; p.out = g.out; p.out2 = g.out2;
   p.geglu = g.geglu;
   if (g.geglu) want_splits = 1;
-  if (g.row_wait) {
-    if (g.taps != 1 || g.stride != 1 || !g.row_ticket) return false;
-    p.row_wait = g.row_wait; p.row_target = g.row_target; p.row_ticket = g.row_ticket;
-  }
   if (!encode_act(&p.ma0, g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_act(&p.ma1, g.a1.base ? g.a1 : g.a0, p.pad, p.Wbox, p.Bbox, p.Rbox, g.stride)) return false;
   if (!encode_w(&p.mb, g.w, g.taps * g.cin, g.N, BN)) return false;

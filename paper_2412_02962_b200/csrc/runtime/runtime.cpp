@@ -76,19 +76,6 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // order on the compute stream, and every kernel orders its global accesses after the previous
 // kernel's completion -- stream order, or griddepcontrol.wait under PDL), so tensors whose live
 // intervals are disjoint share memory: greedy first fit, largest first.  PCPP_MEMPLAN=0 disables it.
-// Attention op i hands its output rows to the out-projection at i + 1 as they complete (row flags),
-// and that GEMM starts without waiting for the attention kernel to finish: it runs on the SMs the
-// attention's last wave leaves idle.  bf16 tensor-core path only (the flags live in those kernels).
-bool early_start_op(const Plan& P, int i) {
-  static const bool on = !getenv("PCPP_EARLY_START") || atoi(getenv("PCPP_EARLY_START")) != 0;
-  // one rank per process only: with loopback virtual ranks the op's launches interleave the ranks, so
-  // a GEMM's stream predecessor is another rank's GEMM, whose completion would no longer imply its own
-  if (!on || !P.use_tc || P.dtype != DT_BF16 || P.nr != 1 || i + 1 >= (int)P.ops.size()) return false;
-  const Op& a = P.ops[i];
-  const Op& g = P.ops[i + 1];
-  return a.k == OP_ATTN && g.k == OP_GEMM && g.in0 == a.out && g.in1 < 0 && !g.geglu;
-}
-
 size_t plan_memory(Plan& P) {
   const int nt = (int)P.td.size();
   std::vector<int> first(nt, 1 << 30), last(nt, -1);
@@ -97,11 +84,6 @@ size_t plan_memory(Plan& P) {
     for (int r : {o.in0, o.in1, o.out, o.out2, o.res, o.tmp})
       if (r >= 0) { first[r] = std::min(first[r], i); last[r] = std::max(last[r], i); }
   }
-  // an out-projection started early behind its attention (early_start_op) writes its output while
-  // the attention's last CTAs still read their queries: the attention's inputs live one op longer
-  for (int i = 0; i + 1 < (int)P.ops.size(); ++i)
-    if (early_start_op(P, i))
-      for (int r : {P.ops[i].in0, P.ops[i].in1}) if (r >= 0) last[r] = std::max(last[r], i + 1);
   std::vector<char> pinned(nt, 0);
   for (int t = 0; t < nt; ++t) pinned[t] = P.td[t].dbl || P.td[t].pad || P.td[t].xdst || last[t] < 0;
   for (const HaloX& h : P.halos) pinned[h.t] = 1;
@@ -225,16 +207,6 @@ pcpp_status plan_allocate(Plan& P) {
       }
     P.ws_elems = std::min<size_t>(8 * mx, (size_t)1 << 28);
     P.ws = (float*)galloc(P.ws_elems * 4);
-  }
-  {
-    P.row_flag_off.assign(P.attns.size(), -1);
-    long long nflags = 0;
-    for (int i = 0; i < (int)P.ops.size(); ++i)
-      if (early_start_op(P, i)) {
-        P.row_flag_off[P.ops[i].xid] = nflags;
-        nflags += (long long)P.nr * (P.attns[P.ops[i].xid].h + 1);
-      }
-    if (nflags) P.row_flags = (unsigned*)galloc((size_t)nflags * 4);   // zeroed
   }
   if (P.xf) {     // cross-attention context: as given, laid out per level, and every layer's keys/values
     P.ctx_f32 = (float*)galloc((size_t)2 * 77 * P.ctx_dim * 4);
@@ -715,7 +687,6 @@ static unsigned op_kind(OpK k) {
 
 void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s);
 bool gemm_tc_supported(const GemmArgs& g);
-bool attn_tc_supported(const AttnArgs& a);
 
 // Per-shape GEMM configuration search on the plan's own buffers (before any graph capture).
 void gemm_tune_load(const char* path);
@@ -784,14 +755,6 @@ pcpp_status context_setup(Plan& P, const float* ctx_host) {
   CK(cudaStreamSynchronize(P.s0));
   P.ctx_set = true;
   return PCPP_OK;
-}
-
-// row flags of attention op oi for virtual rank vr when this run executes both it and its early-started
-// consumer (a partial-mask run -- pcpp_profile's per-kind graphs -- runs them plainly)
-static unsigned* early_row_flags(const Plan& P, size_t oi, unsigned mask, int vr) {
-  if (!P.row_flags || !(mask & K_ATTN) || !(mask & K_GEMM) || !early_start_op(P, (int)oi)) return nullptr;
-  const long long off = P.row_flag_off[P.ops[oi].xid];
-  return off < 0 ? nullptr : P.row_flags + off + (long long)vr * (P.attns[P.ops[oi].xid].h + 1);
 }
 
 pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
@@ -863,14 +826,6 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           if (op.gn_fuse >= 0) {
             g.gn_part = reinterpret_cast<double*>(P.rm[vr].arena + P.off_epart);
             g.gn_slots = &P.gn_slots[(size_t)vr * P.gns.size() + op.gn_fuse];
-          }
-          if (oi > 0 && early_row_flags(P, oi - 1, mask, vr)) {
-            const AttnX& ax = P.attns[P.ops[oi - 1].xid];
-            g.row_wait = early_row_flags(P, oi - 1, mask, vr);
-            g.row_ticket = g.row_wait + ax.h;
-            // arrivals per row: every (head, batch) CTA of each query tile covering it
-            g.row_target = (unsigned)((ax.C / 64) * P.B * (ax.W >= 128 ? (ax.W + 127) / 128 : 1));
-            if (!gemm_tc_supported(g)) { set_error("early start: out-projection off the tensor-core path"); return PCPP_ERR_UNSUPPORTED; }
           }
           if (op.geglu) {    // fused GEGLU epilogue on the tensor-core path, else GEMM into tmp + GEGLU kernel
             g.geglu = 1;
@@ -980,10 +935,6 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           }
           a.nsrc = ns;
           a.ws = P.ws; a.ws_elems = P.ws_elems;
-          if (early_row_flags(P, oi, mask, vr)) {
-            if (!attn_tc_supported(a)) { set_error("early start: attention off the tensor-core path"); return PCPP_ERR_UNSUPPORTED; }
-            a.row_done = early_row_flags(P, oi, mask, vr);
-          }
           launch_attn_tc_or_simt(P, a, s);
         }
         P.launches_per_step += nr;

@@ -139,9 +139,6 @@ struct Plan {
   float* x0_hist = nullptr;     // DPM-Solver++(2M) data-prediction history, [nr][h][W][4] fp32
   double* coef_anc = nullptr;   // ancestral (eta = 1): [S][5] {sqrt(ab), sqrt(1-ab), sqrt(ab'), c_eps, sigma}
   float* ws = nullptr; size_t ws_elems = 0;   // split-K workspace
-  // early start of an attention's out-projection (AttnArgs::row_done / GemmArgs::row_wait): per
-  // attention op, [nr][h + 1] row flags + the consumer's ticket; null when no op qualifies
-  unsigned* row_flags = nullptr; std::vector<long long> row_flag_off;   // per attention xid, -1: off
   std::vector<cudaEvent_t> op_ev; bool op_ev_on = false;   // per-op timing (PCPP_OP_TIMING, pcpp_profile)
   std::vector<void*> gallocs;
 

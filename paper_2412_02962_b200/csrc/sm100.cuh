@@ -367,29 +367,5 @@ template <int N> __device__ __forceinline__ void bulk_wait() {        // the wri
   asm volatile("cp.async.bulk.wait_group %0;" :: "n"(N) : "memory");
 }
 
-// Row-completion flags between a producer kernel and an early-started consumer (gpu scope).
-// Producer: its async-proxy (TMA) stores are complete (bulk_wait<0>); the proxy fence orders them
-// before the generic release.  Consumer: acquire spin (watchdog as mbar_wait), then a proxy fence so
-// the TMA loads it issues next observe the released data.
-__device__ __forceinline__ void flag_release_add(unsigned* f, unsigned v) {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(f), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned flag_acquire(const unsigned* f) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-  return v;
-}
-__device__ __forceinline__ void flag_wait_geq(const unsigned* f, unsigned target) {
-  if (flag_acquire(f) < target) {
-    const long long t0 = clock64();
-    while (flag_acquire(f) < target) {
-      __nanosleep(256);
-      if (clock64() - t0 > 20000000000LL) __trap();
-    }
-  }
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
 }  // namespace sm100
 }  // namespace pcpp
