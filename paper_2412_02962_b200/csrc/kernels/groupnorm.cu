@@ -7,10 +7,12 @@
 // owns fixed 8-channel vectors (16 B) of every token it visits, so its gamma/beta and group ids are
 // registers and each warp reads contiguous 16 B vectors of one token row (coalesced).
 // Deterministic: fixed-order reductions only (loopback == NCCL bitwise, graph == eager bitwise).
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 #include "../common.cuh"
 #include "../kernels.h"
+#include "../sm100.cuh"
 
 namespace pcpp {
 
@@ -46,80 +48,118 @@ __device__ __forceinline__ const T* vptr(const ActView& v, long long rowtok, int
 
 // ---- stats -------------------------------------------------------------------------------------
 // One wave of <= 148 CTAs; CTA `chunk` covers layout tokens [T0, T1) (all (r, b, w) in memory order:
-// address T*C + c).  Thread = (fixed 8-channel vector lane, token lane); token lanes stride by ntl
-// with 4 independent 16 B loads in flight; per-thread fp32 sums over its few tokens, then a
-// fixed-order per-(b, g) reduction in fp64 into the CTA's partial slot partial[chunk][B=2][G][2].
-// The slots are summed by gn_finalize (the same finalize as the GEMM-epilogue-fused statistics).
+// address T*C + c), which are contiguous in memory (per source tensor for a channel concat).  The
+// TMA engine streams them into a ring of STATS_NS shared-memory stages of `ts` tokens (1-D bulk
+// copies: ~96 KB in flight per SM without holding a register -- the register-load version had ~60 KB
+// in flight, stalled on every batch of loads and reached 1.15 TB/s).  Thread = (fixed 8-channel vector
+// lane, token lane) reads its 16-byte vectors of each stage from shared memory; per-thread fp32 sums,
+// then a fixed-order per-(b, g) reduction in fp64 (4 threads per entry, combined in order) into the
+// CTA's partial slot partial[chunk][B=2][G][2].  The slots are summed by gn_finalize (the same
+// finalize as the GEMM-epilogue-fused statistics) or by the apply kernel.
+constexpr int STATS_NS = 4;
+constexpr int STATS_STAGE = 24 * 1024;
+__host__ __device__ __forceinline__ int stats_ts(int C, int es) { const int t = STATS_STAGE / (C * es); return t < 1 ? 1 : t; }
+
 template <typename T>
 __global__ void __launch_bounds__(NT) gn_stats_kernel(const GnStatsArgs a) {
   pdl_trigger();
-  pdl_wait();
-  extern __shared__ float red[];                   // [ntl][nv][2 b][8][2]
+  extern __shared__ __align__(128) uint8_t gsm[];
   const int chunk = blockIdx.x;
-  const int W = a.x0.W, B = a.x0.B, C = a.C;
+  const int W = a.x0.W, B = a.x0.B, C = a.C, c0 = a.c0, c1 = C - a.c0;
+  const int ts = stats_ts(C, (int)sizeof(T));
+  const int SB = ts * C * (int)sizeof(T);
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + STATS_NS * SB);
   const Lanes L = lanes_for(C);
   const int tid = threadIdx.x;
   const int vl = tid % L.nvl, tl = tid / L.nvl;
   const long long ntok = (long long)a.x0.rows * B * W;
   const long long T0 = ntok * chunk / a.nchunk, T1 = ntok * (chunk + 1) / a.nchunk;
-  const int v = vl * L.vpt;                        // vpt == 1 for every supported C
-  if (tl < L.ntl && v < L.nv) {
-    float s[2][8], q[2][8];
+  const int nst = (int)((T1 - T0 + ts - 1) / ts);
+  if (tid == 0) {
+    for (int i = 0; i < STATS_NS; ++i) sm100::mbar_init(&full[i], 1);
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  auto issue = [&](int i) {          // stage i: tokens [T0 + i ts, ...) -> slot i % NS
+    const long long t0 = T0 + (long long)i * ts;
+    const int n = (int)min((long long)ts, T1 - t0);
+    uint8_t* st = gsm + (i % STATS_NS) * SB;
+    uint64_t* bar = &full[i % STATS_NS];
+    sm100::mbar_arrive_expect_tx(bar, (uint32_t)(n * C * sizeof(T)));
+    sm100::bulk_load(st, reinterpret_cast<const T*>(a.x0.base) + t0 * c0, (uint32_t)(n * c0 * sizeof(T)), bar);
+    if (c1) sm100::bulk_load(st + (size_t)ts * c0 * sizeof(T), reinterpret_cast<const T*>(a.x1.base) + t0 * c1,
+                             (uint32_t)(n * c1 * sizeof(T)), bar);
+  };
+  if (tid == 0)
+    for (int i = 0; i < STATS_NS && i < nst; ++i) issue(i);
+  float s[2][8], q[2][8];
 #pragma unroll
-    for (int bb = 0; bb < 2; ++bb)
+  for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) { s[bb][e] = 0.f; q[bb][e] = 0.f; }
-    const int c = v * 8;
-    const bool second = c >= a.c0;
-    const ActView& src = second ? a.x1 : a.x0;
-    const int cc = second ? c - a.c0 : c;
-    long long Tt = T0 + tl;
-    int w = (int)(Tt % W), bq = (int)((Tt / W) % B);
-    constexpr int U = sizeof(T) == 2 ? 8 : 4;      // 16-byte loads in flight per thread
-    for (; Tt < T1; Tt += (long long)U * L.ntl) {
-      float x[U][8];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const long long Tk = Tt + (long long)k * L.ntl;
-        if (Tk < T1) load8(vptr<T>(src, Tk, cc), x[k]);
-        else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[k][e] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
+    for (int e = 0; e < 8; ++e) { s[bb][e] = 0.f; q[bb][e] = 0.f; }
+  const int c = vl * 8;
+  const bool act = tl < L.ntl && vl < L.nv;
+  const bool second = c >= c0;
+  for (int i = 0; i < nst; ++i) {
+    const long long t0 = T0 + (long long)i * ts;
+    const int n = (int)min((long long)ts, T1 - t0);
+    sm100::mbar_wait(&full[i % STATS_NS], (uint32_t)((i / STATS_NS) & 1));
+    if (act) {
+      const T* st = reinterpret_cast<const T*>(gsm + (i % STATS_NS) * SB);
+      const T* src = second ? st + (size_t)ts * c0 + (c - c0) : st + c;
+      const int sC = second ? c1 : c0;
+      for (int t = tl; t < n; t += L.ntl) {
+        float x[8];
+        load8(src + (size_t)t * sC, x);
+        const int bq = (int)(((t0 + t) / W) % B);
         if (bq == 0) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) { s[0][e] += x[k][e]; q[0][e] = fmaf(x[k][e], x[k][e], q[0][e]); }
+          for (int e = 0; e < 8; ++e) { s[0][e] += x[e]; q[0][e] = fmaf(x[e], x[e], q[0][e]); }
         } else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) { s[1][e] += x[k][e]; q[1][e] = fmaf(x[k][e], x[k][e], q[1][e]); }
+          for (int e = 0; e < 8; ++e) { s[1][e] += x[e]; q[1][e] = fmaf(x[e], x[e], q[1][e]); }
         }
-        w += L.ntl;
-        while (w >= W) { w -= W; bq = (bq + 1 == B) ? 0 : bq + 1; }
       }
     }
+    __syncthreads();                               // every thread is done with this slot
+    if (tid == 0 && i + STATS_NS < nst) issue(i + STATS_NS);
+  }
+  // per-thread sums -> smem (the ring is free), then per (b, g, stat) 4 threads in fixed order
+  float* red = reinterpret_cast<float*>(gsm);      // [ntl][nv][2 b][8][2]
+  if (act) {
 #pragma unroll
     for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        red[(((long long)tl * L.nv + v) * 2 + bb) * 16 + e * 2 + 0] = s[bb][e];
-        red[(((long long)tl * L.nv + v) * 2 + bb) * 16 + e * 2 + 1] = q[bb][e];
+        red[(((long long)tl * L.nv + vl) * 2 + bb) * 16 + e * 2 + 0] = s[bb][e];
+        red[(((long long)tl * L.nv + vl) * 2 + bb) * 16 + e * 2 + 1] = q[bb][e];
       }
   }
   __syncthreads();
+  __shared__ double part4[4][128];
   const int cg = C / G;
-  if (tid < 2 * G * 2) {                             // fixed-order per-(b, g, stat) sums -> this CTA's slot
-    const int bb = tid / (2 * G), g = (tid >> 1) % G, k = tid & 1;
+  {
+    const int ent = tid & 127, qq = tid >> 7;       // entry (b, g, stat), quarter of the channel range
+    const int bb = ent / (2 * G), g = (ent >> 1) % G, k = ent & 1;
     double acc = 0.0;
     if (bb < B)
-      for (int c = g * cg; c < (g + 1) * cg; ++c) {
-        const int vv = c / 8, e = c % 8;
+      for (int cc = g * cg + qq; cc < (g + 1) * cg; cc += 4) {
+        const int vv = cc / 8, e = cc % 8;
         for (int l = 0; l < L.ntl; ++l) acc += red[(((long long)l * L.nv + vv) * 2 + bb) * 16 + e * 2 + k];
       }
-    a.partial[(size_t)chunk * 128 + tid] = acc;      // [slot][b][g][2]
+    part4[qq][ent] = acc;
   }
+  __syncthreads();
+  if (tid < 128)
+    a.partial[(size_t)chunk * 128 + tid] = (part4[0][tid] + part4[1][tid]) + (part4[2][tid] + part4[3][tid]);
+}
+
+static size_t stats_smem(int C, int es) {
+  const Lanes L = lanes_for(C);
+  const size_t ring = (size_t)STATS_NS * stats_ts(C, es) * C * es + STATS_NS * 8;
+  const size_t red = (size_t)L.ntl * L.nv * 32 * sizeof(float);
+  return ring > red ? ring : red;
 }
 
 // ---- finalize of the GEMM-fused statistics ------------------------------------------------------
@@ -153,10 +193,8 @@ void launch_gn_finalize(const double* part, int nslots, int B, double* m_out, cu
 
 // stats pass over x (+ x1 for a channel concat) and the finalize of its per-CTA slots
 void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s, bool finalize) {
-  const Lanes L = lanes_for(a.C);
-  const size_t smem = (size_t)L.ntl * L.nv * 32 * sizeof(float);
-  if (a.x0.dtype == DT_F32) launch_pdl(gn_stats_kernel<float>, dim3(a.nchunk), dim3(NT), smem, s, a);
-  else launch_pdl(gn_stats_kernel<bf16>, dim3(a.nchunk), dim3(NT), smem, s, a);
+  if (a.x0.dtype == DT_F32) launch_pdl(gn_stats_kernel<float>, dim3(a.nchunk), dim3(NT), stats_smem(a.C, 4), s, a);
+  else launch_pdl(gn_stats_kernel<bf16>, dim3(a.nchunk), dim3(NT), stats_smem(a.C, 2), s, a);
   if (finalize) launch_gn_finalize(a.partial, a.nchunk, a.x0.B, a.m_out, s);
 }
 
@@ -291,7 +329,107 @@ __global__ void __launch_bounds__(512) gn_apply_wide_kernel(const GnApplyArgs a,
   }
 }
 
+// Streaming apply (single-source input): the CTA's contiguous token range moves through a ring of
+// STATS_NS shared-memory stages by 1-D bulk copies (TMA engine) -- loads in flight while the
+// statistics prologue runs and while earlier stages are transformed -- and every stage is normalised
+// in place and leaves by one bulk store.  Thread = fixed 8-channel vector lane (coefficients in
+// registers) x token lane.  One CTA per SM.
+template <typename T>
+__global__ void __launch_bounds__(NT) gn_apply_bulk_kernel(const GnApplyArgs a) {
+  pdl_trigger();
+  extern __shared__ __align__(128) uint8_t gsm[];
+  __shared__ float mu_s[2 * G], rs_s[2 * G];
+  const int B = a.x0.B, C = a.C, cg = C / G, W = a.x0.W;
+  const int ts = stats_ts(C, (int)sizeof(T));
+  const int SB = ts * C * (int)sizeof(T);
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + STATS_NS * SB);
+  const Lanes L = lanes_for(C);
+  const int tid = threadIdx.x;
+  const int vl = tid % L.nvl, tl = tid / L.nvl;
+  const long long ntok = (long long)a.x0.rows * B * W;
+  const long long T0 = ntok * blockIdx.x / gridDim.x, T1 = ntok * (blockIdx.x + 1) / gridDim.x;
+  const int nst = (int)((T1 - T0 + ts - 1) / ts);
+  if (tid == 0) {
+    for (int i = 0; i < STATS_NS; ++i) sm100::mbar_init(&full[i], 1);
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  const T* xin = reinterpret_cast<const T*>(a.x0.base);
+  T* yout = reinterpret_cast<T*>(a.out.base);
+  auto issue = [&](int i) {
+    const long long t0 = T0 + (long long)i * ts;
+    const int n = (int)min((long long)ts, T1 - t0);
+    uint64_t* bar = &full[i % STATS_NS];
+    sm100::mbar_arrive_expect_tx(bar, (uint32_t)(n * C * sizeof(T)));
+    sm100::bulk_load(gsm + (i % STATS_NS) * SB, xin + t0 * C, (uint32_t)(n * C * sizeof(T)), bar);
+  };
+  if (tid == 0)
+    for (int i = 0; i < STATS_NS && i < nst; ++i) issue(i);
+  const int c = vl * 8;
+  const bool act = tl < L.ntl && vl < L.nv;
+  float ga8[8], be8[8];
+  if (act) { load8(a.gamma + c, ga8); load8(a.beta + c, be8); }
+  gn_prep(a, mu_s, rs_s);                          // overlaps the loads in flight
+  __syncthreads();
+  float A[2][8], Bc[2][8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int g = act ? (c + e) / cg : 0;
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      const int bi = bb < B ? bb : 0;
+      const float rs = rs_s[bi * G + g] * ga8[e];
+      A[bb][e] = rs;
+      Bc[bb][e] = be8[e] - mu_s[bi * G + g] * rs;
+    }
+  }
+  for (int i = 0; i < nst; ++i) {
+    const long long t0 = T0 + (long long)i * ts;
+    const int n = (int)min((long long)ts, T1 - t0);
+    T* st = reinterpret_cast<T*>(gsm + (i % STATS_NS) * SB);
+    sm100::mbar_wait(&full[i % STATS_NS], (uint32_t)((i / STATS_NS) & 1));
+    if (act) {
+      for (int t = tl; t < n; t += L.ntl) {
+        float x[8];
+        T* p = st + (size_t)t * C + c;
+        load8(p, x);
+        const int bq = (int)(((t0 + t) / W) % B);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = fmaf(x[e], bq ? A[1][e] : A[0][e], bq ? Bc[1][e] : Bc[0][e]);
+        if (a.silu) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = std::is_same<T, bf16>::value ? silu_bf16out(x[e]) : silu_f(x[e]);
+        }
+        store8(p, x);
+      }
+    }
+    sm100::fence_proxy_async_smem();               // the generic writes are visible to the bulk store
+    __syncthreads();
+    if (tid == 0) {
+      sm100::bulk_store(yout + t0 * C, st, (uint32_t)(n * C * sizeof(T)));
+      sm100::bulk_commit();
+      if (i >= 1 && i - 1 + STATS_NS < nst) {      // slot of stage i - 1: its store has read it -> refill
+        sm100::bulk_wait_read<1>();
+        issue(i - 1 + STATS_NS);
+      }
+    }
+  }
+  if (tid == 0) sm100::bulk_wait<0>();             // stores complete before the CTA exits
+}
+
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
+  if (!a.x1.base && a.out.dtype == a.x0.dtype && a.out.C == a.C && a.x0.C == a.C) {
+    const long long ntok = (long long)a.x0.rows * a.x0.B * a.x0.W;
+    const int es = a.x0.dtype == DT_F32 ? 4 : 2;
+    const long long stages = (ntok + stats_ts(a.C, es) - 1) / stats_ts(a.C, es);
+    const int grid = (int)std::max<long long>(1, std::min<long long>(148, stages));
+    const size_t smem = (size_t)STATS_NS * stats_ts(a.C, es) * a.C * es + STATS_NS * 8;
+    if (es == 4) launch_pdl(gn_apply_bulk_kernel<float>, dim3(grid), dim3(NT), smem, s, a);
+    else launch_pdl(gn_apply_bulk_kernel<bf16>, dim3(grid), dim3(NT), smem, s, a);
+    return;
+  }
+
   const int nv = a.C / 8;
   const long long ntok = (long long)a.x0.rows * a.x0.B * a.x0.W;
   long long blocks = (ntok * nv + 512 * 4 - 1) / (512 * 4);
@@ -303,9 +441,11 @@ void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {
   else launch_pdl(gn_apply_wide_kernel<bf16, bf16>, dim3((unsigned)blocks), dim3(512), 0, s, a, lanes);
 }
 
-void gn_init() {   // dynamic smem: ntl * nv * 32 floats <= 66 KB (ntl * nv <= 512)
-  cudaFuncSetAttribute(gn_stats_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-  cudaFuncSetAttribute(gn_stats_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+void gn_init() {   // dynamic smem: the stage ring (<= 4 x 24 KB + barriers) or the reduction scratch (<= 64 KB)
+  cudaFuncSetAttribute(gn_stats_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  cudaFuncSetAttribute(gn_stats_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  cudaFuncSetAttribute(gn_apply_bulk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  cudaFuncSetAttribute(gn_apply_bulk_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
 }
 
 }  // namespace pcpp

@@ -367,5 +367,18 @@ template <int N> __device__ __forceinline__ void bulk_wait() {        // the wri
   asm volatile("cp.async.bulk.wait_group %0;" :: "n"(N) : "memory");
 }
 
+// 1-D bulk copy global -> this CTA's shared memory (TMA engine), completion counted in bytes on an
+// mbarrier; src / dst 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// 1-D bulk copy this CTA's shared memory -> global (bulk-group completion: bulk_commit / bulk_wait*)
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(dst), "r"(smem_u32(src)), "r"(bytes) : "memory");
+}
+
 }  // namespace sm100
 }  // namespace pcpp
