@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(AttnCfg<NWG>::THREADS, NWG == 2 ? 1 : 2) attn_
         if (row == 0) {
           sm100::tma_store_4d(&p.mo, Qs, head * 64, (qt % p.nWt) * p.Wbox, b, (qt / p.nWt) * p.Rbox);
           sm100::bulk_commit();
-          sm100::bulk_wait<0>();
+          sm100::bulk_wait_read<0>();       // smem may be released; the grid completes after its stores
         }
       } else if (row < p.Wbox * p.Rbox && r < p.h && w < p.W) {
         const float inv = 1.f / l;

@@ -12,6 +12,7 @@
 //   two warps per TMEM lane quadrant (warp % 4), each taking every other 32-column chunk.
 // * SWIZZLE_128B K-major smem tiles, STAGES-deep mbarrier ring between TMA and MMA.
 #include <cuda.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -395,7 +396,7 @@ __device__ __forceinline__ void gemm_csplit_reduce(const TcGemmParams& p, uint8_
       sm100::bulk_commit();
     }
   }
-  if (lane == 0) sm100::bulk_wait<0>();
+  if (lane == 0) sm100::bulk_wait_read<0>();
   if (ST) gn_cta_finish(p, gacc, stg_all);
 }
 
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[a]);
     }
-    if (p.tma_st && lane == 0) sm100::bulk_wait<0>();   // staged stores complete before exit
+    if (p.tma_st && lane == 0) sm100::bulk_wait_read<0>();   // staged stores have read smem (they complete with the grid)
     if (threadIdx.x == 64) trace_stamp(p, 5);
     if (ST && p.csplit <= 1) gn_cta_finish(p, gacc, stg_all);
   }
@@ -826,7 +827,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc2_kernel(const __grid_
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(sm100::leader_addr(&tempty[a]));
     }
-    if (p.tma_st && lane == 0) sm100::bulk_wait<0>();
+    if (p.tma_st && lane == 0) sm100::bulk_wait_read<0>();
     if (ST) gn_cta_finish(p, gacc, stg_all);
   }
   sm100::fence_before();
@@ -1137,15 +1138,21 @@ void gemm_tc_autotune(const GemmArgs& g, cudaStream_t s) {
         sa.m_out = reinterpret_cast<double*>(g.gn_part) + (size_t)sa.nchunk * 128;
       }
       if (!launch_gemm_tc_cfg(g, s, bn, S, pair)) continue;      // warm
-      cudaEventRecord(e0, s);
-      for (int r = 0; r < 3; ++r) {
-        launch_gemm_tc_cfg(g, s, bn, S, pair);
-        if (stats_pass) launch_gn_stats(sa, s);
+      // best of 2 trials of 5 back-to-back launches (3 single-trial launches left the table noisy:
+      // re-tuning moved the step by +-0.1 ms)
+      float ms = 1e30f;
+      for (int trial = 0; trial < 2; ++trial) {
+        cudaEventRecord(e0, s);
+        for (int r = 0; r < 5; ++r) {
+          launch_gemm_tc_cfg(g, s, bn, S, pair);
+          if (stats_pass) launch_gn_stats(sa, s);
+        }
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        ms = std::min(ms, t * 3.f / 5.f);      // per 3 launches (the unit the log line divides by)
       }
-      cudaEventRecord(e1, s);
-      cudaEventSynchronize(e1);
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, e0, e1);
       if (ms < best_ms * 0.97f) { best_ms = ms; best = GemmChoice{bn, S, pair}; }
     }
   }

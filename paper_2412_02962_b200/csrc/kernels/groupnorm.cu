@@ -199,22 +199,24 @@ void launch_gn_stats(const GnStatsArgs& a, cudaStream_t s, bool finalize) {
 }
 
 // ---- apply -------------------------------------------------------------------------------------
-// the fresh local sums m[b][g][k] from the producer's slots (nslots <= GN_MERGE_MAX_SLOTS = 48): 4
-// threads per entry, each summing every 4th slot in order, then the 4 in fixed order (deterministic);
-// CTA 0 publishes them to m_write
+// the fresh local sums m[b][g][k] from the producer's slots (any count; one per producer CTA, <= 148 at
+// n = 1): 4 threads per entry, thread q summing slots q, q + 4, ... in order (12 loads in flight per
+// batch), then the 4 in fixed order (deterministic); CTA 0 publishes them to m_write.  Summing here
+// replaces a gn_finalize launch (one dependent launch per GroupNorm layer).
 __device__ __forceinline__ void gn_slots_sum(const GnApplyArgs& a, double* mf) {
   __shared__ double red[4][128];
   const int e = threadIdx.x & 127, q = threadIdx.x >> 7;     // NT = 512: q in [0, 4)
-  // every load of the thread in flight at once (nslots <= 48: at most 12), then summed in slot order
-  double v[12];
-#pragma unroll
-  for (int i = 0; i < 12; ++i) {
-    const int k = q + 4 * i;
-    v[i] = k < a.nslots ? __ldcg(a.part + (size_t)k * 128 + e) : 0.0;
-  }
   double acc = 0.0;
+  for (int base = 0; base < a.nslots; base += 48) {
+    double v[12];
 #pragma unroll
-  for (int i = 0; i < 12; ++i) acc += v[i];
+    for (int i = 0; i < 12; ++i) {
+      const int k = base + q + 4 * i;
+      v[i] = k < a.nslots ? __ldcg(a.part + (size_t)k * 128 + e) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) acc += v[i];
+  }
   red[q][e] = acc;
   __syncthreads();
   if (threadIdx.x < 128) {
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(NT) gn_apply_bulk_kernel(const GnApplyArgs a) 
       }
     }
   }
-  if (tid == 0) sm100::bulk_wait<0>();             // stores complete before the CTA exits
+  if (tid == 0) sm100::bulk_wait_read<0>();        // the stores have read smem (they complete with the grid)
 }
 
 void launch_gn_apply(const GnApplyArgs& a, cudaStream_t s) {

@@ -872,19 +872,18 @@ pcpp_status run_step(Plan& P, float* latent, int sync, int par, unsigned mask) {
           return a;
         };
         {
-          // few partial slots (small producer grids, the n >= 4 shapes) and no synchronous exchange of
-          // this step's sums: the apply kernel sums the slots itself (no finalize launch) and publishes
-          // m[par]; the asynchronous exchange of m[par] then follows the apply
-          constexpr int MERGE_MAX_SLOTS = 48;
+          // no synchronous exchange of this step's sums: the apply kernel sums the producer's partial
+          // slots itself (no finalize launch) and publishes m[par]; the asynchronous exchange of m[par]
+          // then follows the apply
           const bool can_merge = n == 1 || !sync;
           std::vector<int> merged(nr, 0);
           for (int vr = 0; vr < nr && do_op; ++vr) {
             const int slots = P.gn_slots[(size_t)vr * P.gns.size() + op.xid];
-            if (slots > 0 && can_merge && slots <= MERGE_MAX_SLOTS) { merged[vr] = slots; continue; }
+            if (slots > 0 && can_merge) { merged[vr] = slots; continue; }
             if (slots > 0)
               launch_gn_finalize(reinterpret_cast<const double*>(P.rm[vr].arena + P.off_epart), slots, P.B,
                                  reinterpret_cast<double*>(P.rm[vr].arena + gx.off_m[par]), s);
-            else if (can_merge && gx.nchunk <= MERGE_MAX_SLOTS) {
+            else if (can_merge) {
               launch_gn_stats(stats_args(vr), s, false);
               merged[vr] = -gx.nchunk;              // slots of the stats kernel
             } else
