@@ -310,7 +310,106 @@ __global__ void __launch_bounds__(256) conv_out_v3_kernel(const ActView in, cons
   }
 }
 
+// conv_out with warp-level tensor-core MMAs (bf16 in, Cin -> 4, fp32 out): out[t][o] = bias[o] +
+// sum_{tap, c} x[t + tap][c] W[o][tap C + c] as 16-token x 8-output (4 real) tiles of
+// mma.sync.m16n8k16 (fp32 accumulation).  The fp32 weights are split w = hi + lo (both bf16, lo =
+// bf16(w - hi)) and each K step issues the two MMAs, so the weights keep ~16 mantissa bits (x is bf16
+// exactly).  The K index inside a 16-channel step is permuted so that lane (g, t) holds channels
+// 4t .. 4t + 3 of its tokens: one 8-byte load per token row (full 32-byte sectors) and one 8-byte smem
+// load per weight half; A and B use the same permutation, so the sum is unchanged.  CTA = 4 warps =
+// 64 consecutive output tokens of one (row, batch); the 3x3 reuse is served by L1.
+constexpr int COUT_TOK = 64;
+__device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__global__ void __launch_bounds__(128) conv_out_mma_kernel(const ActView in, const float* __restrict__ w,
+                                                           const float* __restrict__ bias, const ActView out) {
+  pdl_trigger();
+  extern __shared__ __align__(16) uint8_t csm[];
+  const int C = in.C, K = 9 * C, Kp = K + 16;                 // row pad: conflict-free 8-byte reads
+  bf16* whi = reinterpret_cast<bf16*>(csm);                   // [4][Kp]
+  bf16* wlo = whi + 4 * Kp;
+  for (int i = threadIdx.x; i < K / 4; i += blockDim.x * 4) {    // weights (static: before the PDL wait), float4
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k4 = i + u * blockDim.x;                      // float4 index within a row of K / 4
+      if (k4 >= K / 4) break;
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(w + (size_t)o * K) + k4);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bf16 h = __float2bfloat16_rn(vv[e]);
+          whi[o * Kp + 4 * k4 + e] = h;
+          wlo[o * Kp + 4 * k4 + e] = __float2bfloat16_rn(vv[e] - __bfloat162float(h));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nwt = (out.W + COUT_TOK - 1) / COUT_TOK;
+  const int wt = blockIdx.x % nwt, rb = blockIdx.x / nwt;
+  const int b = rb % out.B, r = rb / out.B;
+  const int wA = wt * COUT_TOK + warp * 16 + g;               // this lane's two tokens: wA, wA + 8
+  const bf16* x = reinterpret_cast<const bf16*>(in.base);
+  float d[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool bl = g < 4;                                      // B columns (outputs) 4..7 are zero
+  const uint2 z2 = make_uint2(0u, 0u);
+  for (int tap = 0; tap < 9; ++tap) {
+    const int dr = tap / 3 - 1, dw = tap % 3 - 1;
+    const int w0 = wA + dw, w1 = wA + 8 + dw;
+    const bool v0 = w0 >= 0 && w0 < in.W, v1 = w1 >= 0 && w1 < in.W;
+    const bf16* row = x + (((long long)(r + dr) * in.B + b) * in.W) * C + 4 * t;
+    const bf16* p0 = row + (long long)w0 * C;
+    const bf16* p1 = row + (long long)w1 * C;
+    const bf16* ph = whi + g * Kp + tap * C + 4 * t;
+    const bf16* pl = wlo + g * Kp + tap * C + 4 * t;
+    // batches of U K steps: all loads of a batch are issued before its MMAs (the MMAs chain through d,
+    // so the compiler would otherwise issue each load just before its use)
+    constexpr int U = 8;
+    for (int cb = 0; cb < C; cb += 16 * U) {
+      uint2 a0[U], a1[U], bh[U], bo[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c0 = cb + 16 * u;
+        const bool kin = c0 < C;
+        a0[u] = (kin && v0) ? __ldg(reinterpret_cast<const uint2*>(p0 + c0)) : z2;
+        a1[u] = (kin && v1) ? __ldg(reinterpret_cast<const uint2*>(p1 + c0)) : z2;
+        bh[u] = (kin && bl) ? *reinterpret_cast<const uint2*>(ph + c0) : z2;
+        bo[u] = (kin && bl) ? *reinterpret_cast<const uint2*>(pl + c0) : z2;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t af[4] = {a0[u].x, a1[u].x, a0[u].y, a1[u].y};   // (g, k 2t..), (g+8, ..), (g, k 2t+8..), (g+8, ..)
+        mma_bf16_16816(d, af, bh[u].x, bh[u].y);
+        mma_bf16_16816(d, af, bo[u].x, bo[u].y);
+      }
+    }
+  }
+  if (t < 2) {                                                // outputs 2t, 2t + 1 of tokens wA, wA + 8
+    const float b0 = bias[2 * t], b1 = bias[2 * t + 1];
+    float* po = reinterpret_cast<float*>(out.base) + (((long long)r * out.B + b) * out.W) * 4 + 2 * t;
+    if (wA < out.W) *reinterpret_cast<float2*>(po + (long long)wA * 4) = make_float2(d[0] + b0, d[1] + b1);
+    if (wA + 8 < out.W) *reinterpret_cast<float2*>(po + (long long)(wA + 8) * 4) = make_float2(d[2] + b0, d[3] + b1);
+  }
+}
+
 void launch_conv_out(const ActView& in, const float* w, const float* bias, const ActView& out, cudaStream_t s) {
+  if (in.dtype == DT_BF16 && in.C % 16 == 0 && out.C == 4 && (size_t)(9 * in.C + 16) * 16 <= 100 * 1024) {
+    const int nwt = (out.W + COUT_TOK - 1) / COUT_TOK;
+    const size_t smem = (size_t)(9 * in.C + 16) * 4 * 2 * 2;
+    static bool attr = false;
+    if (!attr) { cudaFuncSetAttribute(conv_out_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024); attr = true; }
+    launch_pdl(conv_out_mma_kernel, dim3((unsigned)(out.rows * out.B * nwt)), dim3(128), smem, s, in, w, bias, out);
+    return;
+  }
+
   if (in.dtype == DT_BF16 && in.C % 8 == 0 && out.C == 4 && out.W % 4 == 0 && (size_t)in.C * 9 * 16 <= 48 * 1024) {
     const long long ngroups = (long long)out.rows * out.B * (out.W / 4);
     const long long blocks = std::min<long long>((ngroups + 7) / 8, 148 * 2);
